@@ -1,0 +1,134 @@
+/*
+ * libcmb200 -- C ABI of the B200-native cross-map hot path.
+ *
+ * The reference (`crossmap`, /root/reference/pkg) is pure Python with no FFI;
+ * each entry point below replaces one hot function of that package and is
+ * bound from Python with ctypes.  Plain pointers and
+ * sizes only; every host buffer is caller-owned, read or written during the
+ * call and never retained.  Calls block until results are in the caller's
+ * buffers.  Calls on one device are serialised internally; calls on
+ * different devices may run concurrently from different host threads.
+ *
+ * Arrays are row-major.  "len" is a series length in samples.  Returns 0 on
+ * success or a negative CMB_ERR_* code; cmb_last_error() then holds a
+ * one-line, thread-local message.
+ */
+#ifndef CMB200_H
+#define CMB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CMB_OK 0
+#define CMB_ERR_PARAM (-1)       /* -> ParameterError      (errors.py:8)  */
+#define CMB_ERR_TOO_SHORT (-2)   /* -> SeriesTooShortError (errors.py:12) */
+#define CMB_ERR_ZERO_VAR (-3)    /* -> ZeroVarianceError   (errors.py:16) */
+#define CMB_ERR_CUDA (-10)       /* -> DeviceError (CrossmapError subclass) */
+#define CMB_ERR_NCCL (-11)
+#define CMB_ERR_UNSUPPORTED (-12)
+
+/* rho layouts for cmb_xmap* */
+#define CMB_LAYOUT_LIB_MAJOR 0    /* rho[lib * N + tgt]  (SkillMatrix.rho, ccm.py:56-83) */
+#define CMB_LAYOUT_TGT_MAJOR 1    /* rho[tgt * N + lib]  (native kernel layout) */
+
+/* Library version, lockstep with the Python package __version__ (0.1.0 -> 100). */
+int cmb_version(void);
+/* Message for the most recent failing call on this thread. */
+const char* cmb_last_error(void);
+/* Number of visible CUDA devices. */
+int cmb_device_count(int* n);
+/* Diagnostics since the last call (then reset): out[0] kNN rows re-selected
+ * by the exact fp64 fallback, out[1] rows checked, out[2] kernel launches
+ * issued by the library (host-side count), out[3..] reserved.              */
+int cmb_diagnostics(int dev, int64_t* out, int n);
+/* Release every device buffer held by the library. */
+int cmb_shutdown(void);
+
+/* ---- kNN stage (knn.py) -------------------------------------------------- */
+
+/* pairwise_distances (knn.py:97-128): D[n][n] squared distances between all
+ * delay vectors, n = len - (E-1)*tau, float64, reference operation order.   */
+int cmb_pairwise_distances(int dev, const double* x, int64_t len, int E, int tau,
+                           double* D_out);
+
+/* partial_sort_topk (knn.py:144-177): per row the k smallest entries of
+ * D[n][n] over columns j != i, ascending, ties to the smaller column.       */
+int cmb_partial_sort_topk(int dev, const double* D, int64_t n, int k,
+                          double* d_out, int64_t* idx_out);
+
+/* normalize_to_weights (knn.py:180-202): sq[n][k] ascending squared
+ * distances -> simplex weights.                                             */
+int cmb_normalize_weights(int dev, const double* sq, int64_t n, int k, double* w_out);
+
+/* build_knn_table (knn.py:205-217): fused embedding + distance + exact
+ * top-k + weights, the n x n matrix never materialised.  n = len-(E-1)*tau.
+ * d_out (nullable) receives the selected squared distances.                 */
+int cmb_knn_table(int dev, const double* x, int64_t len, int E, int tau, int k,
+                  int64_t* idx_out, double* w_out, double* d_out);
+
+/* ---- prediction stage (prediction.py) ------------------------------------ */
+
+/* PearsonAggregate.from_arrays (prediction.py:45-55):
+ * agg_out = {count, mean_a, mean_b, m2_a, m2_b, comoment}.                  */
+int cmb_pearson(int dev, const double* a, const double* b, int64_t n, double* agg_out);
+
+/* lookup_batch (prediction.py:122-161): targets Y[M][len] through one table
+ * (idx[n][k], w[n][k], sample offset (E-1)*tau).  rho_out[M] (NaN when
+ * undefined), pred_out[M][n] (nullable).                                    */
+int cmb_lookup(int dev, const int64_t* idx, const double* w, int64_t n, int k, int offset,
+               const double* Y, int64_t len, int64_t M, double* rho_out, double* pred_out);
+
+/* simplex_self_predict (prediction.py:164-182). NaN if undefined.           */
+int cmb_simplex(int dev, const double* x, int64_t len, int E, int tau, int Tp, double* rho_out);
+
+/* _self_skill_curve + optimal_embedding (prediction.py:197-262), batched over
+ * N series X[N][len].  rho_out[N][E_max] (NaN undefined); estar_out[N]
+ * (0 = undefined: constant series or an undefined curve point).            */
+int cmb_edim(int dev, const double* X, int64_t N, int64_t len, int E_max, int tau, int Tp,
+             double* rho_out, int32_t* estar_out);
+
+/* ---- all-to-all cross map (ccm.py:94-151) -------------------------------- */
+
+/* rho over every ordered (library, target) pair; the library is embedded at
+ * the target's E (estar[tgt]); Tp = 0 lookup; estar[i] == 0 marks series i
+ * undefined (its row and column are NaN).  X[N][len] float32 samples.
+ * stats_out (nullable, 8 doubles): seconds {tables, lookup, total},
+ * tables_built, distinct_E, pairs, 0, 0.                                    */
+int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* estar, int tau,
+             float* rho_out, int layout, double* stats_out);
+
+/* Device-resident shard of cmb_xmap for the multi-GPU driver: X_dev[N][ld]
+ * (float32, on `dev`), libraries [lib_begin, lib_end); writes
+ * rhoT_dev[tgt * ldr + (lib - lib_begin)] (target-major).  `stream` is a
+ * cudaStream_t (NULL = the library's stream); the call returns after the
+ * work completes.                                                           */
+int cmb_xmap_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld,
+                 const int32_t* estar, int tau, int64_t lib_begin, int64_t lib_end,
+                 float* rhoT_dev, int64_t ldr, void* stream, double* stats_out);
+
+/* Device-resident edim: X_dev[N][ld] float32; rho_dev[N][E_max] float64,
+ * estar_dev[N] int32.                                                       */
+int cmb_edim_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld, int E_max,
+                 int tau, int Tp, double* rho_dev, int32_t* estar_dev, void* stream);
+
+/* ---- convergence sweep (no reference implementation) ------- */
+
+/* For each library size sizes[s] and sample q: neighbours restricted to the
+ * sampled library points lib_pts[s][q][0..sizes[s]) (sorted point indices,
+ * offsets into lib_pts given by lib_off[s]), prediction of every embedded
+ * point of every target, Pearson skill.  Series X[N][len]; pairs
+ * (lib_ids[p], tgt_ids[p]) at dimension E_pair[p].
+ * rho_out[P][n_sizes][samples] (NaN undefined).                             */
+int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int tau,
+                        const int32_t* lib_ids, const int32_t* tgt_ids, const int32_t* E_pair,
+                        int64_t P, const int32_t* sizes, int n_sizes, int samples,
+                        const int32_t* lib_pts, const int64_t* lib_off, double* rho_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CMB200_H */

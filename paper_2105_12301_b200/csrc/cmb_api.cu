@@ -1,0 +1,707 @@
+// extern "C" boundary of libcmb200: validation, device contexts, staging of
+// host buffers, and the cross-map driver that sequences the kernels.
+#include "cmb_common.cuh"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace cmb {
+
+// ---------------------------------------------------------------- errors
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  set_error("CUDA error %s (%s) at %s:%d: %s", cudaGetErrorName(e), cudaGetErrorString(e), file,
+            line, what);
+  return CMB_ERR_CUDA;
+}
+
+static std::atomic<long long> g_launches{0};
+void count_launch(int n) { g_launches += n; }
+
+// ---------------------------------------------------------------- device context
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  ~DevBuf() {}
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max(bytes, (size_t)256);
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+enum BufId {
+  B_X64, B_X32, B_ERR, B_MEAN, B_Y, B_SLOT_TGT, B_SLOT_E, B_OBS_S, B_OBS_SS, B_OBS_C, B_LIBROWS,
+  B_LIBCOL, B_TAB, B_COUNTER, B_RHOT, B_RHO, B_PART, B_LAST, B_LMEAN, B_A, B_B, B_C, B_D, B_E,
+  B_DIAG, B_EST, B_NBUF
+};
+
+struct Ctx {
+  int dev = 0;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  DevBuf buf[B_NBUF];
+  bool ready = false;
+};
+
+static std::mutex g_ctx_mu;
+static std::vector<std::unique_ptr<Ctx>> g_ctx;
+
+static int get_ctx(int dev, Ctx** out) {
+  int n = 0;
+  CMB_CUDA(cudaGetDeviceCount(&n));
+  if (dev < 0 || dev >= n) {
+    set_error("device %d not available (%d visible)", dev, n);
+    return CMB_ERR_PARAM;
+  }
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  if ((int)g_ctx.size() < n) g_ctx.resize(n);
+  if (!g_ctx[dev]) g_ctx[dev].reset(new Ctx());
+  Ctx* c = g_ctx[dev].get();
+  if (!c->ready) {
+    CMB_CUDA(cudaSetDevice(dev));
+    CMB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CMB_CUDA(c->buf[B_DIAG].ensure(8 * sizeof(unsigned long long)));
+    CMB_CUDA(cudaMemset(c->buf[B_DIAG].p, 0, 8 * sizeof(unsigned long long)));
+    c->dev = dev;
+    c->ready = true;
+  }
+  *out = c;
+  return CMB_OK;
+}
+
+#define CMB_CTX(dev)                                  \
+  Ctx* ctx = nullptr;                                 \
+  {                                                   \
+    int _r = get_ctx((dev), &ctx);                    \
+    if (_r) return _r;                                \
+  }                                                   \
+  std::lock_guard<std::mutex> _lock(ctx->mu);         \
+  CMB_CUDA(cudaSetDevice(ctx->dev));                  \
+  cudaStream_t st = ctx->stream;
+
+#define CMB_TRY(call)               \
+  do {                              \
+    int _r = (call);                \
+    if (_r) return _r;              \
+  } while (0)
+
+static int too_short(int64_t len, int E, int tau, int64_t n) {
+  set_error("series of length %lld yields %lld embedded points for E=%d, tau=%d; neighbor search needs at least %d",
+            (long long)len, (long long)n, E, tau, E + 2);
+  return CMB_ERR_TOO_SHORT;
+}
+
+// valid_count (series.py:84-98)
+static int check_valid_count(int64_t len, int E, int tau) {
+  if (len < 1) {
+    set_error("a series needs at least one observation");
+    return CMB_ERR_TOO_SHORT;
+  }
+  const int64_t n = len - (int64_t)(E - 1) * tau;
+  if (n < E + 2) return too_short(len, E, tau, n);
+  return CMB_OK;
+}
+
+static int check_spec(int E, int tau) {
+  CMB_PARAM(tau >= 1, "lag must be >= 1, got %d", tau);
+  CMB_PARAM(E >= 1, "embedding dimension must be >= 1, got %d", E);
+  return CMB_OK;
+}
+
+// ---------------------------------------------------------------- kNN (RAW) via the sweep
+static int knn_raw(Ctx* ctx, cudaStream_t st, const double* x_dev, const float* x32_dev,
+                   const float* err_dev, int64_t len, int E, int tau, int k, int64_t* idx_dev,
+                   double* w_dev, double* d_dev) {
+  KnnArgs a;
+  memset(&a, 0, sizeof(a));
+  a.x32 = x32_dev;
+  a.x64 = x_dev;
+  a.ld = len;
+  a.nlib = 1;
+  a.L = (int)len;
+  a.tau = tau;
+  a.e_hi = E;
+  a.need = 1u << (E - 1);
+  a.mode = KNN_RAW;
+  a.k_raw = k;
+  a.rows_per_block = 64;
+  a.nrb = (int)((len + 63) / 64);
+  a.err_m = err_dev;
+  a.raw_idx = idx_dev;
+  a.raw_w = w_dev;
+  a.raw_d = d_dev;
+  a.diag = ctx->buf[B_DIAG].as<unsigned long long>();
+  CMB_CUDA(launch_knn_sweep(a, st));
+  return CMB_OK;
+}
+
+// upload a float64 series batch and derive its float32 copy + rounding error
+static int stage_series64(Ctx* ctx, cudaStream_t st, const double* X, int64_t N, int64_t len) {
+  CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * len));
+  CMB_CUDA(ctx->buf[B_X32].ensure(sizeof(float) * N * len + 256));
+  CMB_CUDA(ctx->buf[B_ERR].ensure(sizeof(float) * N));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X64].p, X, sizeof(double) * N * len, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(launch_demote(ctx->buf[B_X64].as<double>(), N, len, ctx->buf[B_X32].as<float>(),
+                         ctx->buf[B_ERR].as<float>(), st));
+  return CMB_OK;
+}
+
+// ---------------------------------------------------------------- self-prediction sweep (EDIM)
+static int edim_core(Ctx* ctx, cudaStream_t st, const float* x32, const double* x64,
+                     const float* err, int64_t N, int64_t len, int64_t ld, int E_hi, uint32_t need,
+                     int tau, int Tp, double* rho_dev, int32_t* estar_dev) {
+  const int L = (int)(len - Tp);
+  const int rpb = 64;
+  const int nrb = (L + rpb - 1) / rpb;
+  // batch libraries to bound the partial-moment buffer (~256 MB)
+  int64_t batch = std::max<int64_t>(1, (256ll << 20) / ((int64_t)nrb * E_hi * 5 * 8));
+  batch = std::min<int64_t>(batch, N);
+  CMB_CUDA(ctx->buf[B_PART].ensure(sizeof(double) * batch * nrb * E_hi * 5));
+  CMB_CUDA(ctx->buf[B_LAST].ensure(sizeof(int) * batch));
+  CMB_CUDA(ctx->buf[B_LMEAN].ensure(sizeof(double) * batch));
+  for (int64_t b0 = 0; b0 < N; b0 += batch) {
+    const int64_t nb = std::min(batch, N - b0);
+    KnnArgs a;
+    memset(&a, 0, sizeof(a));
+    a.x32 = x32 + b0 * ld;
+    a.x64 = x64 + b0 * ld;
+    a.ld = ld;
+    a.nlib = (int)nb;
+    a.L = L;
+    a.tau = tau;
+    a.e_hi = E_hi;
+    a.need = need;
+    a.mode = KNN_EDIM;
+    a.rows_per_block = rpb;
+    a.nrb = nrb;
+    a.err_m = err ? err + b0 : nullptr;
+    a.Tp = Tp;
+    a.part = ctx->buf[B_PART].as<double>();
+    a.last_change = ctx->buf[B_LAST].as<int>();
+    a.mean = ctx->buf[B_LMEAN].as<double>();
+    a.diag = ctx->buf[B_DIAG].as<unsigned long long>();
+    CMB_CUDA(launch_knn_sweep(a, st));
+    CMB_CUDA(launch_edim_finalize(a.part, a.last_change, (int)nb, nrb, E_hi, L, tau, Tp,
+                                  rho_dev + b0 * E_hi, estar_dev ? estar_dev + b0 : nullptr,
+                                  nullptr, st));
+  }
+  return CMB_OK;
+}
+
+// ---------------------------------------------------------------- cross-map driver
+struct XmapStats {
+  double t_tables = 0, t_lookup = 0, t_total = 0;
+  double tables = 0, distinct = 0, pairs = 0;
+};
+
+static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64_t T, int64_t ld,
+                     const int32_t* estar, int tau, int64_t lib_begin, int64_t lib_end, float* rhoT,
+                     int64_t ldr, XmapStats* stats) {
+  CMB_PARAM(tau >= 1, "tau must be >= 1, got %d", tau);
+  CMB_PARAM(lib_begin >= 0 && lib_begin <= lib_end && lib_end <= N, "bad library range [%lld, %lld)",
+            (long long)lib_begin, (long long)lib_end);
+  CMB_PARAM(T <= 65535, "series length %lld exceeds the 16-bit table format", (long long)T);
+  // ---- group targets by E* (ccm.py:123-127)
+  std::vector<std::vector<int>> by_e(CMB_SWEEP_MAX_E + 1);
+  for (int64_t t = 0; t < N; ++t) {
+    const int e = estar[t];
+    if (e == 0) continue;
+    CMB_PARAM(e >= 1 && e <= CMB_SWEEP_MAX_E, "dimension %d outside [1, %d]", e, CMB_SWEEP_MAX_E);
+    by_e[e].push_back((int)t);
+  }
+  std::vector<int32_t> slot_tgt, slot_E;
+  LookupArgs la;
+  memset(&la, 0, sizeof(la));
+  uint32_t need = 0;
+  int e_hi = 0, max_rec = 0;
+  for (int e = 1; e <= CMB_SWEEP_MAX_E; ++e) {
+    if (by_e[e].empty()) continue;
+    CMB_TRY(check_valid_count(T, e, tau));
+    const int g = la.ngroups++;
+    la.g_E[g] = e;
+    la.g_blk0[g] = (int)(slot_tgt.size() / 32);
+    const size_t padded = (by_e[e].size() + 31) / 32 * 32;
+    la.g_nblk[g] = (int)(padded / 32);
+    for (size_t q = 0; q < padded; ++q) {
+      slot_tgt.push_back(q < by_e[e].size() ? by_e[e][q] : -1);
+      slot_E.push_back(e);
+    }
+    need |= 1u << (e - 1);
+    e_hi = e;
+    max_rec = std::max(max_rec, rec_bytes(e + 1));
+  }
+  std::vector<int32_t> lib_rows;
+  std::vector<int64_t> lib_col;
+  for (int64_t l = lib_begin; l < lib_end; ++l)
+    if (estar[l] != 0) {
+      lib_rows.push_back((int32_t)l);
+      lib_col.push_back(l - lib_begin);
+    }
+  const int64_t ncols = lib_end - lib_begin;
+  CMB_CUDA(launch_fill_nan(rhoT, N, ncols, ldr, st));
+  if (la.ngroups == 0 || lib_rows.empty()) return CMB_OK;
+  const int stage = lookup_stage_bytes((int)T, max_rec);
+  if (stage == 0) {
+    set_error("series length %lld too long for the shared-memory resident lookup", (long long)T);
+    return CMB_ERR_UNSUPPORTED;
+  }
+
+  // ---- device staging
+  const int64_t slots = (int64_t)slot_tgt.size();
+  const int64_t ldy = slots;
+  CMB_CUDA(ctx->buf[B_SLOT_TGT].ensure(4 * slots));
+  CMB_CUDA(ctx->buf[B_SLOT_E].ensure(4 * slots));
+  CMB_CUDA(ctx->buf[B_OBS_S].ensure(8 * slots));
+  CMB_CUDA(ctx->buf[B_OBS_SS].ensure(8 * slots));
+  CMB_CUDA(ctx->buf[B_OBS_C].ensure(slots));
+  CMB_CUDA(ctx->buf[B_Y].ensure(sizeof(float) * T * ldy));
+  CMB_CUDA(ctx->buf[B_MEAN].ensure(8 * N));
+  CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * ld));
+  CMB_CUDA(ctx->buf[B_LIBROWS].ensure(4 * lib_rows.size()));
+  CMB_CUDA(ctx->buf[B_LIBCOL].ensure(8 * lib_col.size()));
+  CMB_CUDA(ctx->buf[B_COUNTER].ensure(16));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_SLOT_TGT].p, slot_tgt.data(), 4 * slots, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_SLOT_E].p, slot_E.data(), 4 * slots, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_LIBROWS].p, lib_rows.data(), 4 * lib_rows.size(), cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_LIBCOL].p, lib_col.data(), 8 * lib_col.size(), cudaMemcpyHostToDevice, st));
+  CMB_CUDA(launch_series_stats(X, N, T, ld, ctx->buf[B_MEAN].as<double>(), st));
+  CMB_CUDA(launch_build_targets(X, ld, ctx->buf[B_MEAN].as<double>(), ctx->buf[B_SLOT_TGT].as<int32_t>(),
+                                slots, (int)T, ctx->buf[B_Y].as<float>(), ldy, st));
+  CMB_CUDA(launch_obs_moments(ctx->buf[B_Y].as<float>(), ldy, (int)T, tau, ctx->buf[B_SLOT_E].as<int32_t>(),
+                              slots, ctx->buf[B_OBS_S].as<double>(), ctx->buf[B_OBS_SS].as<double>(),
+                              ctx->buf[B_OBS_C].as<uint8_t>(), st));
+  CMB_CUDA(launch_promote(X, N, T, ld, ctx->buf[B_X64].as<double>(), st));
+
+  // ---- library chunks: tables for every needed E, then the lookup
+  size_t per_lib = 0;
+  size_t tab_off[CMB_SWEEP_MAX_E + 2] = {0};
+  for (int g = 0; g < la.ngroups; ++g) {
+    const int e = la.g_E[g];
+    per_lib += (size_t)(T - (int64_t)(e - 1) * tau) * rec_bytes(e + 1);
+  }
+  const int LS = 64;
+  const size_t budget = (size_t)6 << 30;
+  int64_t C = (int64_t)(budget / std::max<size_t>(per_lib, 1));
+  C = std::max<int64_t>(LS, C / LS * LS);
+  C = std::min<int64_t>(C, ((int64_t)lib_rows.size() + LS - 1) / LS * LS);
+  CMB_CUDA(ctx->buf[B_TAB].ensure(per_lib * C + 256));
+  {
+    size_t o = 0;
+    for (int g = 0; g < la.ngroups; ++g) {
+      const int e = la.g_E[g];
+      tab_off[e] = o;
+      o += (size_t)C * (T - (int64_t)(e - 1) * tau) * rec_bytes(e + 1);
+    }
+  }
+
+  cudaEvent_t ev[3];
+  for (auto& e : ev) CMB_CUDA(cudaEventCreate(&e));
+  float ms_tab = 0, ms_look = 0;
+  const int rpb = 64;
+  for (int64_t c0 = 0; c0 < (int64_t)lib_rows.size(); c0 += C) {
+    const int64_t nc = std::min<int64_t>(C, (int64_t)lib_rows.size() - c0);
+    KnnArgs a;
+    memset(&a, 0, sizeof(a));
+    a.x32 = X;
+    a.x64 = ctx->buf[B_X64].as<double>();
+    a.ld = ld;
+    a.lib_rows = ctx->buf[B_LIBROWS].as<int32_t>() + c0;
+    a.nlib = (int)nc;
+    a.L = (int)T;
+    a.tau = tau;
+    a.e_hi = e_hi;
+    a.need = need;
+    a.mode = KNN_TABLE;
+    a.rows_per_block = rpb;
+    a.nrb = (int)((T + rpb - 1) / rpb);
+    for (int g = 0; g < la.ngroups; ++g) a.tab[la.g_E[g]] = ctx->buf[B_TAB].as<uint8_t>() + tab_off[la.g_E[g]];
+    a.diag = ctx->buf[B_DIAG].as<unsigned long long>();
+    CMB_CUDA(cudaEventRecord(ev[0], st));
+    CMB_CUDA(launch_knn_sweep(a, st));
+    CMB_CUDA(cudaEventRecord(ev[1], st));
+
+    la.Y = ctx->buf[B_Y].as<float>();
+    la.ldy = ldy;
+    la.T = (int)T;
+    la.tau = tau;
+    la.slot_tgt = ctx->buf[B_SLOT_TGT].as<int32_t>();
+    la.obs_s = ctx->buf[B_OBS_S].as<double>();
+    la.obs_ss = ctx->buf[B_OBS_SS].as<double>();
+    la.obs_const = ctx->buf[B_OBS_C].as<uint8_t>();
+    for (int g = 0; g < la.ngroups; ++g) la.tab[la.g_E[g]] = a.tab[la.g_E[g]];
+    la.nlib = (int)nc;
+    la.lib_col = ctx->buf[B_LIBCOL].as<int64_t>() + c0;
+    la.LS = LS;
+    la.n_lsub = (int)((nc + LS - 1) / LS);
+    int64_t items = 0;
+    for (int g = 0; g < la.ngroups; ++g) {
+      la.g_item0[g] = items;
+      items += (int64_t)la.n_lsub * la.g_nblk[g];
+    }
+    la.g_item0[la.ngroups] = items;
+    la.n_items = items;
+    la.counter = ctx->buf[B_COUNTER].as<int>();
+    la.rhoT = rhoT;
+    la.ldr = ldr;
+    la.stage_bytes = stage;
+    CMB_CUDA(cudaMemsetAsync(la.counter, 0, sizeof(int), st));
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->dev);
+    CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(items, dev_sms), st));
+    CMB_CUDA(cudaEventRecord(ev[2], st));
+    CMB_CUDA(cudaEventSynchronize(ev[2]));
+    float a_ms = 0, b_ms = 0;
+    CMB_CUDA(cudaEventElapsedTime(&a_ms, ev[0], ev[1]));
+    CMB_CUDA(cudaEventElapsedTime(&b_ms, ev[1], ev[2]));
+    ms_tab += a_ms;
+    ms_look += b_ms;
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  if (stats) {
+    stats->t_tables = ms_tab * 1e-3;
+    stats->t_lookup = ms_look * 1e-3;
+    stats->tables = (double)lib_rows.size() * la.ngroups;
+    stats->distinct = la.ngroups;
+    int64_t tg = 0;
+    for (int g = 0; g < la.ngroups; ++g) tg += (int64_t)by_e[la.g_E[g]].size();
+    stats->pairs = (double)lib_rows.size() * (double)tg;
+  }
+  return CMB_OK;
+}
+
+}  // namespace cmb
+
+using namespace cmb;
+
+// =====================================================================================
+extern "C" {
+
+int cmb_version(void) { return 100; }
+
+const char* cmb_last_error(void) { return g_err; }
+
+int cmb_device_count(int* n) {
+  CMB_CUDA(cudaGetDeviceCount(n));
+  return CMB_OK;
+}
+
+int cmb_diagnostics(int dev, int64_t* out, int n) {
+  CMB_CTX(dev);
+  unsigned long long h[8];
+  CMB_CUDA(cudaMemcpyAsync(h, ctx->buf[B_DIAG].p, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaMemsetAsync(ctx->buf[B_DIAG].p, 0, sizeof(h), st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  h[2] = (unsigned long long)g_launches.exchange(0);
+  for (int q = 0; q < n && q < 8; ++q) out[q] = (int64_t)h[q];
+  return CMB_OK;
+}
+
+int cmb_shutdown(void) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  for (auto& c : g_ctx) {
+    if (!c) continue;
+    std::lock_guard<std::mutex> l(c->mu);
+    cudaSetDevice(c->dev);
+    for (auto& b : c->buf) b.release();
+    if (c->stream) cudaStreamDestroy(c->stream);
+    c->stream = nullptr;
+    c->ready = false;
+  }
+  g_ctx.clear();
+  return CMB_OK;
+}
+
+int cmb_pairwise_distances(int dev, const double* x, int64_t len, int E, int tau, double* D_out) {
+  CMB_TRY(check_spec(E, tau));
+  const int64_t n = len - (int64_t)(E - 1) * tau;
+  if (n < 2) {
+    set_error("series of length %lld yields %lld embedded points for E=%d, tau=%d; pairwise distances need at least 2",
+              (long long)len, (long long)n, E, tau);
+    return CMB_ERR_TOO_SHORT;
+  }
+  CMB_CTX(dev);
+  CMB_CUDA(ctx->buf[B_A].ensure(8 * len));
+  CMB_CUDA(ctx->buf[B_B].ensure(8 * n * n));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_A].p, x, 8 * len, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(launch_pairwise(ctx->buf[B_A].as<double>(), (int)n, E, tau, ctx->buf[B_B].as<double>(), st));
+  CMB_CUDA(cudaMemcpyAsync(D_out, ctx->buf[B_B].p, 8 * n * n, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  return CMB_OK;
+}
+
+int cmb_partial_sort_topk(int dev, const double* D, int64_t n, int k, double* d_out, int64_t* idx_out) {
+  CMB_PARAM(k >= 1 && k <= n - 1, "neighbor count must lie in [1, %lld], got %d", (long long)(n - 1), k);
+  CMB_PARAM(n <= 16384, "partial_sort_topk supports n <= 16384, got %lld", (long long)n);
+  CMB_CTX(dev);
+  CMB_CUDA(ctx->buf[B_A].ensure(8 * n * n));
+  CMB_CUDA(ctx->buf[B_B].ensure(8 * n * k));
+  CMB_CUDA(ctx->buf[B_C].ensure(8 * n * k));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_A].p, D, 8 * n * n, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(launch_topk_rows(ctx->buf[B_A].as<double>(), (int)n, k, ctx->buf[B_B].as<double>(),
+                            ctx->buf[B_C].as<int64_t>(), st));
+  CMB_CUDA(cudaMemcpyAsync(d_out, ctx->buf[B_B].p, 8 * n * k, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaMemcpyAsync(idx_out, ctx->buf[B_C].p, 8 * n * k, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  return CMB_OK;
+}
+
+int cmb_normalize_weights(int dev, const double* sq, int64_t n, int k, double* w_out) {
+  CMB_PARAM(k >= 1 && n >= 0, "expected an n x k distance array, got (%lld, %d)", (long long)n, k);
+  if (n == 0) return CMB_OK;
+  CMB_CTX(dev);
+  CMB_CUDA(ctx->buf[B_A].ensure(8 * n * k));
+  CMB_CUDA(ctx->buf[B_B].ensure(8 * n * k));
+  CMB_CUDA(ctx->buf[B_C].ensure(16));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_A].p, sq, 8 * n * k, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemsetAsync(ctx->buf[B_C].p, 0, 4, st));
+  CMB_CUDA(launch_weights(ctx->buf[B_A].as<double>(), n, k, ctx->buf[B_B].as<double>(), ctx->buf[B_C].as<int>(), st));
+  int flags = 0;
+  CMB_CUDA(cudaMemcpyAsync(&flags, ctx->buf[B_C].p, 4, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaMemcpyAsync(w_out, ctx->buf[B_B].p, 8 * n * k, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  CMB_PARAM(!(flags & 1), "squared distances must be >= 0");
+  CMB_PARAM(!(flags & 2), "distance rows must be ascending");
+  return CMB_OK;
+}
+
+int cmb_knn_table(int dev, const double* x, int64_t len, int E, int tau, int k, int64_t* idx_out,
+                  double* w_out, double* d_out) {
+  CMB_TRY(check_spec(E, tau));
+  CMB_TRY(check_valid_count(len, E, tau));
+  const int64_t n = len - (int64_t)(E - 1) * tau;
+  CMB_PARAM(k >= 1 && k <= n - 1, "neighbor count must lie in [1, %lld], got %d", (long long)(n - 1), k);
+  CMB_CTX(dev);
+  CMB_TRY(stage_series64(ctx, st, x, 1, len));
+  CMB_CUDA(ctx->buf[B_A].ensure(8 * n * k));
+  CMB_CUDA(ctx->buf[B_B].ensure(8 * n * k));
+  CMB_CUDA(ctx->buf[B_C].ensure(8 * n * k));
+  if (E <= CMB_SWEEP_MAX_E && k + 1 <= 32) {
+    CMB_TRY(knn_raw(ctx, st, ctx->buf[B_X64].as<double>(), ctx->buf[B_X32].as<float>(),
+                    ctx->buf[B_ERR].as<float>(), len, E, tau, k, ctx->buf[B_A].as<int64_t>(),
+                    ctx->buf[B_B].as<double>(), ctx->buf[B_C].as<double>()));
+  } else {
+    // wide k: materialised distances + per-row sort + weights (same semantics)
+    CMB_PARAM(n <= 16384, "k > 31 tables support n <= 16384, got %lld", (long long)n);
+    CMB_CUDA(ctx->buf[B_D].ensure(8 * n * n));
+    CMB_CUDA(ctx->buf[B_E].ensure(16));
+    CMB_CUDA(launch_pairwise(ctx->buf[B_X64].as<double>(), (int)n, E, tau, ctx->buf[B_D].as<double>(), st));
+    CMB_CUDA(launch_topk_rows(ctx->buf[B_D].as<double>(), (int)n, k, ctx->buf[B_C].as<double>(),
+                              ctx->buf[B_A].as<int64_t>(), st));
+    CMB_CUDA(cudaMemsetAsync(ctx->buf[B_E].p, 0, 4, st));
+    CMB_CUDA(launch_weights(ctx->buf[B_C].as<double>(), n, k, ctx->buf[B_B].as<double>(), ctx->buf[B_E].as<int>(), st));
+  }
+  CMB_CUDA(cudaMemcpyAsync(idx_out, ctx->buf[B_A].p, 8 * n * k, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaMemcpyAsync(w_out, ctx->buf[B_B].p, 8 * n * k, cudaMemcpyDeviceToHost, st));
+  if (d_out) CMB_CUDA(cudaMemcpyAsync(d_out, ctx->buf[B_C].p, 8 * n * k, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  return CMB_OK;
+}
+
+int cmb_pearson(int dev, const double* a, const double* b, int64_t n, double* agg_out) {
+  CMB_PARAM(n >= 0, "negative length");
+  if (n == 0) {
+    for (int q = 0; q < 6; ++q) agg_out[q] = 0.0;
+    return CMB_OK;
+  }
+  CMB_CTX(dev);
+  CMB_CUDA(ctx->buf[B_A].ensure(8 * n));
+  CMB_CUDA(ctx->buf[B_B].ensure(8 * n));
+  CMB_CUDA(ctx->buf[B_C].ensure(64));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_A].p, a, 8 * n, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_B].p, b, 8 * n, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(launch_pearson(ctx->buf[B_A].as<double>(), ctx->buf[B_B].as<double>(), n, ctx->buf[B_C].as<double>(), st));
+  CMB_CUDA(cudaMemcpyAsync(agg_out, ctx->buf[B_C].p, 48, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  return CMB_OK;
+}
+
+int cmb_lookup(int dev, const int64_t* idx, const double* w, int64_t n, int k, int offset,
+               const double* Y, int64_t len, int64_t M, double* rho_out, double* pred_out) {
+  CMB_PARAM(n >= 1 && k >= 1 && offset >= 0, "bad table shape (%lld, %d)", (long long)n, k);
+  CMB_PARAM(len >= n + offset, "target has %lld samples; table needs at least %lld", (long long)len,
+            (long long)(n + offset));
+  if (M == 0) return CMB_OK;
+  CMB_CTX(dev);
+  CMB_CUDA(ctx->buf[B_A].ensure(8 * n * k));
+  CMB_CUDA(ctx->buf[B_B].ensure(8 * n * k));
+  CMB_CUDA(ctx->buf[B_C].ensure(8 * M * len));
+  CMB_CUDA(ctx->buf[B_D].ensure(8 * M * n));
+  CMB_CUDA(ctx->buf[B_E].ensure(8 * M));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_A].p, idx, 8 * n * k, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_B].p, w, 8 * n * k, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_C].p, Y, 8 * M * len, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(launch_lookup64(ctx->buf[B_A].as<int64_t>(), ctx->buf[B_B].as<double>(), n, k, offset,
+                           ctx->buf[B_C].as<double>(), len, M, ctx->buf[B_D].as<double>(),
+                           ctx->buf[B_E].as<double>(), st));
+  CMB_CUDA(cudaMemcpyAsync(rho_out, ctx->buf[B_E].p, 8 * M, cudaMemcpyDeviceToHost, st));
+  if (pred_out) CMB_CUDA(cudaMemcpyAsync(pred_out, ctx->buf[B_D].p, 8 * M * n, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  return CMB_OK;
+}
+
+int cmb_simplex(int dev, const double* x, int64_t len, int E, int tau, int Tp, double* rho_out) {
+  CMB_TRY(check_spec(E, tau));
+  CMB_PARAM(Tp >= 1, "prediction horizon must be >= 1, got %d", Tp);
+  if (len <= Tp) {
+    set_error("series of length %lld cannot support horizon %d", (long long)len, Tp);
+    return CMB_ERR_TOO_SHORT;
+  }
+  CMB_TRY(check_valid_count(len - Tp, E, tau));
+  CMB_PARAM(E <= CMB_SWEEP_MAX_E, "embedding dimension %d exceeds the supported %d", E, CMB_SWEEP_MAX_E);
+  CMB_CTX(dev);
+  CMB_TRY(stage_series64(ctx, st, x, 1, len));
+  CMB_CUDA(ctx->buf[B_RHO].ensure(8 * E));
+  CMB_TRY(edim_core(ctx, st, ctx->buf[B_X32].as<float>(), ctx->buf[B_X64].as<double>(),
+                    ctx->buf[B_ERR].as<float>(), 1, len, len, E, 1u << (E - 1), tau, Tp,
+                    ctx->buf[B_RHO].as<double>(), nullptr));
+  std::vector<double> r(E);
+  CMB_CUDA(cudaMemcpyAsync(r.data(), ctx->buf[B_RHO].p, 8 * E, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  *rho_out = r[E - 1];
+  return CMB_OK;
+}
+
+int cmb_edim(int dev, const double* X, int64_t N, int64_t len, int E_max, int tau, int Tp,
+             double* rho_out, int32_t* estar_out) {
+  CMB_PARAM(E_max >= 1, "dimension bound must be >= 1, got %d", E_max);
+  CMB_PARAM(Tp >= 1, "prediction horizon must be >= 1, got %d", Tp);
+  CMB_PARAM(tau >= 1, "lag must be >= 1, got %d", tau);
+  CMB_PARAM(E_max <= CMB_SWEEP_MAX_E, "dimension bound %d exceeds the supported %d", E_max, CMB_SWEEP_MAX_E);
+  if (len <= Tp) {
+    set_error("series of length %lld cannot support horizon %d", (long long)len, Tp);
+    return CMB_ERR_TOO_SHORT;
+  }
+  CMB_TRY(check_valid_count(len - Tp, E_max, tau));
+  if (N == 0) return CMB_OK;
+  CMB_CTX(dev);
+  CMB_TRY(stage_series64(ctx, st, X, N, len));
+  CMB_CUDA(ctx->buf[B_RHO].ensure(8 * N * E_max));
+  CMB_CUDA(ctx->buf[B_EST].ensure(4 * N));
+  const uint32_t need = (E_max >= 32) ? 0xffffffffu : ((1u << E_max) - 1);
+  CMB_TRY(edim_core(ctx, st, ctx->buf[B_X32].as<float>(), ctx->buf[B_X64].as<double>(),
+                    ctx->buf[B_ERR].as<float>(), N, len, len, E_max, need, tau, Tp,
+                    ctx->buf[B_RHO].as<double>(), ctx->buf[B_EST].as<int32_t>()));
+  CMB_CUDA(cudaMemcpyAsync(rho_out, ctx->buf[B_RHO].p, 8 * N * E_max, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaMemcpyAsync(estar_out, ctx->buf[B_EST].p, 4 * N, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  return CMB_OK;
+}
+
+int cmb_edim_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld, int E_max, int tau,
+                 int Tp, double* rho_dev, int32_t* estar_dev, void* stream) {
+  CMB_PARAM(E_max >= 1 && E_max <= CMB_SWEEP_MAX_E, "dimension bound %d outside [1, %d]", E_max, CMB_SWEEP_MAX_E);
+  CMB_PARAM(Tp >= 1 && tau >= 1, "bad Tp/tau");
+  if (len <= Tp) {
+    set_error("series of length %lld cannot support horizon %d", (long long)len, Tp);
+    return CMB_ERR_TOO_SHORT;
+  }
+  CMB_TRY(check_valid_count(len - Tp, E_max, tau));
+  CMB_CTX(dev);
+  if (stream) st = (cudaStream_t)stream;
+  CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * ld));
+  CMB_CUDA(launch_promote(X_dev, N, len, ld, ctx->buf[B_X64].as<double>(), st));
+  const uint32_t need = (E_max >= 32) ? 0xffffffffu : ((1u << E_max) - 1);
+  CMB_TRY(edim_core(ctx, st, X_dev, ctx->buf[B_X64].as<double>(), nullptr, N, len, ld, E_max, need,
+                    tau, Tp, rho_dev, estar_dev));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  return CMB_OK;
+}
+
+int cmb_xmap_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld, const int32_t* estar,
+                 int tau, int64_t lib_begin, int64_t lib_end, float* rhoT_dev, int64_t ldr, void* stream,
+                 double* stats_out) {
+  CMB_CTX(dev);
+  if (stream) st = (cudaStream_t)stream;
+  XmapStats s;
+  cudaEvent_t e0, e1;
+  CMB_CUDA(cudaEventCreate(&e0));
+  CMB_CUDA(cudaEventCreate(&e1));
+  CMB_CUDA(cudaEventRecord(e0, st));
+  CMB_TRY(xmap_core(ctx, st, X_dev, N, len, ld, estar, tau, lib_begin, lib_end, rhoT_dev, ldr, &s));
+  CMB_CUDA(cudaEventRecord(e1, st));
+  CMB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (stats_out) {
+    const double v[8] = {s.t_tables, s.t_lookup, ms * 1e-3, s.tables, s.distinct, s.pairs, 0, 0};
+    memcpy(stats_out, v, sizeof(v));
+  }
+  return CMB_OK;
+}
+
+int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* estar, int tau,
+             float* rho_out, int layout, double* stats_out) {
+  CMB_PARAM(layout == CMB_LAYOUT_LIB_MAJOR || layout == CMB_LAYOUT_TGT_MAJOR, "bad layout %d", layout);
+  CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
+  CMB_CTX(dev);
+  const int64_t ldr = (N + 3) / 4 * 4;
+  CMB_CUDA(ctx->buf[B_X32].ensure(sizeof(float) * N * len + 256));
+  CMB_CUDA(ctx->buf[B_RHOT].ensure(sizeof(float) * N * ldr));
+  cudaEvent_t e0, e1;
+  CMB_CUDA(cudaEventCreate(&e0));
+  CMB_CUDA(cudaEventCreate(&e1));
+  CMB_CUDA(cudaEventRecord(e0, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X32].p, X, sizeof(float) * N * len, cudaMemcpyHostToDevice, st));
+  XmapStats s;
+  CMB_TRY(xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
+                    ctx->buf[B_RHOT].as<float>(), ldr, &s));
+  if (layout == CMB_LAYOUT_TGT_MAJOR) {
+    CMB_CUDA(cudaMemcpy2DAsync(rho_out, sizeof(float) * N, ctx->buf[B_RHOT].p, sizeof(float) * ldr,
+                               sizeof(float) * N, N, cudaMemcpyDeviceToHost, st));
+  } else {
+    CMB_CUDA(ctx->buf[B_RHO].ensure(sizeof(float) * N * ldr));
+    CMB_CUDA(launch_transpose_f32(ctx->buf[B_RHOT].as<float>(), N, N, ldr, ctx->buf[B_RHO].as<float>(), ldr, st));
+    CMB_CUDA(cudaMemcpy2DAsync(rho_out, sizeof(float) * N, ctx->buf[B_RHO].p, sizeof(float) * ldr,
+                               sizeof(float) * N, N, cudaMemcpyDeviceToHost, st));
+  }
+  CMB_CUDA(cudaEventRecord(e1, st));
+  CMB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (stats_out) {
+    const double v[8] = {s.t_tables, s.t_lookup, ms * 1e-3, s.tables, s.distinct, s.pairs, 0, 0};
+    memcpy(stats_out, v, sizeof(v));
+  }
+  return CMB_OK;
+}
+
+int cmb_ccm_convergence(int, const double*, int64_t, int64_t, int, const int32_t*, const int32_t*,
+                        const int32_t*, int64_t, const int32_t*, int, int, const int32_t*,
+                        const int64_t*, double*) {
+  set_error("cmb_ccm_convergence is not implemented yet");
+  return CMB_ERR_UNSUPPORTED;
+}
+
+}  // extern "C"

@@ -1,0 +1,108 @@
+// Kernel argument blocks and launchers shared by the C-ABI layer.
+#pragma once
+
+#include "cmb_common.cuh"
+
+namespace cmb {
+
+// host-side count of kernel launches issued by the library (diagnostics[2])
+void count_launch(int n = 1);
+
+enum KnnMode { KNN_TABLE = 0, KNN_EDIM = 1, KNN_RAW = 2 };
+
+struct KnnArgs {
+  const float* x32;         // series-major samples [*][ld] (sweep)
+  const double* x64;        // same samples in float64 [*][ld] (exact re-rank, predictions)
+  int64_t ld;
+  const int32_t* lib_rows;  // series row of each library slot (nullable = identity)
+  int nlib;
+  int L;                    // library length: T (cross map) or T - Tp (self prediction)
+  int tau;
+  int e_hi;                 // largest E swept
+  uint32_t need;            // bit E-1 set when dimension E is emitted
+  int mode;                 // KnnMode
+  int k_raw;                // KNN_RAW: neighbour count (else E + 1)
+  int rows_per_block;
+  int nrb;                  // row blocks per library
+  const float* err_m;       // per library slot: max |x32 - x64| (nullable = 0)
+  // KNN_TABLE: per E base pointer of [nlib][n_E][rec_bytes(E+1)]
+  uint8_t* tab[CMB_SWEEP_MAX_E + 1];
+  // KNN_EDIM
+  int Tp;
+  double* part;             // [nlib][nrb][e_hi][5] shifted moments
+  int* last_change;         // [nlib] last index where the series changes value
+  double* mean;             // [nlib] series mean (Pearson shift)
+  // KNN_RAW (single E = e_hi)
+  int64_t* raw_idx;
+  double* raw_w;
+  double* raw_d;
+  unsigned long long* diag; // [0] exact fallbacks, [1] rows checked
+};
+
+int sweep_width(int e_hi);
+cudaError_t launch_knn_sweep(const KnnArgs& a, cudaStream_t st);
+cudaError_t launch_edim_finalize(const double* part, const int* last_change, int nlib, int nrb,
+                                 int e_hi, int L, int tau, int Tp, double* rho, int32_t* estar,
+                                 const int32_t* valid, cudaStream_t st);
+
+// ------------------------------------------------------------------ K3 lookup
+#define CMB_MAX_GROUPS 32
+
+struct LookupArgs {
+  const float* Y;            // [T][ldy] time-major targets, grouped by E, centred
+  int64_t ldy;
+  int T;
+  int tau;
+  int ngroups;
+  int g_E[CMB_MAX_GROUPS];   // dimension of each group
+  int g_blk0[CMB_MAX_GROUPS];// first 32-target block of each group
+  int g_nblk[CMB_MAX_GROUPS];// blocks per group
+  int64_t g_item0[CMB_MAX_GROUPS + 1];
+  const int32_t* slot_tgt;   // [slots] rho row (target id) or -1 for padding
+  const double* obs_s;       // [slots] sum of the centred observed segment
+  const double* obs_ss;      // [slots] sum of squares
+  const uint8_t* obs_const;  // [slots] 1 when the observed segment is constant
+  const uint8_t* tab[CMB_SWEEP_MAX_E + 1];  // per E: [nlib][n_E][rec]
+  int nlib;                  // libraries in this chunk
+  const int64_t* lib_col;    // [nlib] rho column of each chunk library
+  int LS;                    // libraries per work item
+  int n_lsub;
+  int64_t n_items;
+  int* counter;              // work-item counter, zero before launch
+  float* rhoT;               // rho_T[tgt * ldr + col]
+  int64_t ldr;
+  int stage_bytes;           // per-warp table staging slot
+};
+
+constexpr int kLookupWarps = 16;
+int lookup_smem_bytes(int T, int stage_bytes);
+int lookup_stage_bytes(int T, int max_rec_bytes);  // 0 when T does not fit
+cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st);
+
+// ------------------------------------------------------------------ helpers (utils.cu)
+cudaError_t launch_series_stats(const float* x32, int64_t N, int64_t T, int64_t ld, double* mean,
+                                cudaStream_t st);
+cudaError_t launch_promote(const float* x32, int64_t N, int64_t T, int64_t ld, double* x64,
+                           cudaStream_t st);
+cudaError_t launch_demote(const double* x64, int64_t N, int64_t T, float* x32, float* err_m,
+                          cudaStream_t st);
+cudaError_t launch_build_targets(const float* x32, int64_t ld, const double* mean,
+                                 const int32_t* slot_tgt, int64_t slots, int T, float* Y,
+                                 int64_t ldy, cudaStream_t st);
+cudaError_t launch_obs_moments(const float* Y, int64_t ldy, int T, int tau, const int32_t* slot_E,
+                               int64_t slots, double* s, double* ss, uint8_t* cst, cudaStream_t st);
+cudaError_t launch_fill_nan(float* p, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
+cudaError_t launch_pairwise(const double* x, int n, int E, int tau, double* D, cudaStream_t st);
+cudaError_t launch_topk_rows(const double* D, int n, int k, double* d_out, int64_t* i_out,
+                             cudaStream_t st);
+cudaError_t launch_weights(const double* sq, int64_t n, int k, double* w, int* flags,
+                           cudaStream_t st);
+cudaError_t launch_pearson(const double* a, const double* b, int64_t n, double* agg,
+                           cudaStream_t st);
+cudaError_t launch_lookup64(const int64_t* idx, const double* w, int64_t n, int k, int offset,
+                            const double* Y, int64_t len, int64_t M, double* pred,
+                            double* rho, cudaStream_t st);
+cudaError_t launch_transpose_f32(const float* src, int64_t rows, int64_t cols, int64_t lds,
+                                 float* dst, int64_t ldd, cudaStream_t st);
+
+}  // namespace cmb

@@ -1,0 +1,260 @@
+// K3: cross-map lookup with fused Pearson skill -- the hot kernel of xmap.
+//
+// Replaces lookup_batch (prediction.py:122-161) and PearsonAggregate
+// (prediction.py:25-79) as called from ccm_pairwise (ccm.py:131-149): for
+// every (library, target) pair, predictions
+//     p_t = sum_k w[t,k] * y[row[t,k]],  row = idx + (E-1)*tau
+// for all n_E embedded points, and rho(y[(E-1)tau + t], p_t).  Only rho
+// leaves the SM.
+//
+// B200 mapping.  A CTA keeps one block of 32 targets (all with the same E*)
+// resident in shared memory, time-major: tgt[t][lane] -- T = 1,450 samples x
+// 128 B = 185.6 KB of the 227 KB -- so every gathered row is one
+// conflict-free 128-byte shared-memory wavefront (lane = target).  Its 16
+// warps each stream their own libraries' neighbour tables (records of k
+// fp32 weights + k u16 rows) from L2/HBM into a 2-slot shared-memory ring
+// with cp.async.bulk (TMA bulk copies) completing on an mbarrier, so table
+// bytes are fetched once per (library, target block) and read back as
+// broadcast 16-byte shared loads.  Skill is accumulated per lane in fp32 over
+// a staging slot and folded into fp64; rho is evaluated in fp64 against the
+// precomputed observed-segment moments.
+//
+// Work items are (E group, library sub-range, target block), handed out by
+// an atomic counter so concurrently running CTAs share the same libraries'
+// tables in L2.
+#include "cmb_common.cuh"
+#include "kernels.cuh"
+
+namespace cmb {
+
+namespace {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct WarpStream {
+  const uint8_t* base;  // table of the warp's first library
+  int n;                // records per library
+  int R;                // record bytes
+  int RS;               // records per stage
+  int nst;              // stages per library
+  int total;            // stages in the stream
+};
+
+__device__ __forceinline__ void issue_stage(const WarpStream& ws, int q, uint8_t* slot, uint64_t* bar) {
+  const int l = q / ws.nst, s = q - l * ws.nst;
+  const int r0 = s * ws.RS;
+  const int nrec = min(ws.RS, ws.n - r0);
+  const uint32_t bytes = (uint32_t)(nrec * ws.R);
+  const uint8_t* src = ws.base + ((size_t)l * ws.n + r0) * ws.R;
+  mbar_expect_tx(bar, bytes);
+  bulk_g2s(slot, src, bytes, bar);
+}
+
+template <int K>
+__device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float* __restrict__ tgt,
+                                               uint8_t* ring, uint64_t* bars, uint32_t& qglob,
+                                               int E, int lib0, int nl, int slot_base) {
+  constexpr int KP4 = rec_kp4(K), KP8 = rec_kp8(K);
+  constexpr int R = 4 * KP4 + 2 * KP8;
+  const int lane = lane_id();
+  const int n = a.T - (E - 1) * a.tau;
+  const int off = (E - 1) * a.tau;
+  WarpStream ws;
+  ws.base = a.tab[E] + (size_t)lib0 * n * R;
+  ws.n = n;
+  ws.R = R;
+  ws.RS = a.stage_bytes / R;
+  ws.nst = (n + ws.RS - 1) / ws.RS;
+  ws.total = nl * ws.nst;
+
+  // observed-segment moments of this lane's target
+  const int slot = slot_base + lane;
+  const int tgt_id = a.slot_tgt[slot];
+  const double So = a.obs_s[slot], Soo = a.obs_ss[slot];
+  const bool ocst = a.obs_const[slot] != 0;
+  const float* __restrict__ tcol = tgt + lane;
+
+  // prologue: two stages in flight
+  if (lane == 0) {
+    for (int q = 0; q < 2 && q < ws.total; ++q) {
+      const uint32_t g = qglob + q;
+      issue_stage(ws, q, ring + (g & 1) * a.stage_bytes, bars + (g & 1));
+    }
+  }
+  __syncwarp();
+
+  double Sp = 0.0, Spp = 0.0, Sop = 0.0;
+  for (int q = 0; q < ws.total; ++q) {
+    const uint32_t g = qglob + q;
+    uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
+    mbar_wait(bars + (g & 1), (g >> 1) & 1);
+    const int l = q / ws.nst, s = q - l * ws.nst;
+    const int r0 = s * ws.RS;
+    const int nrec = min(ws.RS, n - r0);
+    float sp = 0.f, spp = 0.f, sop = 0.f;
+#pragma unroll 2
+    for (int r = 0; r < nrec; ++r) {
+      const uint8_t* rec = slotp + r * R;
+      float wv[KP4];
+      uint32_t rv[KP8 / 2];
+#pragma unroll
+      for (int c = 0; c < KP4 / 4; ++c) {
+        const float4 v = reinterpret_cast<const float4*>(rec)[c];
+        wv[4 * c] = v.x; wv[4 * c + 1] = v.y; wv[4 * c + 2] = v.z; wv[4 * c + 3] = v.w;
+      }
+#pragma unroll
+      for (int c = 0; c < KP8 / 8; ++c) {
+        const uint4 v = reinterpret_cast<const uint4*>(rec + 4 * KP4)[c];
+        rv[4 * c] = v.x; rv[4 * c + 1] = v.y; rv[4 * c + 2] = v.z; rv[4 * c + 3] = v.w;
+      }
+      const float o = tcol[(off + r0 + r) * 32];
+      float p = 0.f;
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const uint32_t row = (rv[kk >> 1] >> (16 * (kk & 1))) & 0xffffu;
+        p = __fmaf_rn(wv[kk], tcol[row * 32], p);
+      }
+      sp += p;
+      spp = __fmaf_rn(p, p, spp);
+      sop = __fmaf_rn(o, p, sop);
+    }
+    Sp += sp;
+    Spp += spp;
+    Sop += sop;
+    __syncwarp();
+    if (lane == 0 && q + 2 < ws.total) issue_stage(ws, q + 2, slotp, bars + (g & 1));
+    if (s == ws.nst - 1) {
+      // library complete: skill of (library, this lane's target)
+      const double nn = (double)n;
+      const double m2o = Soo - So * So / nn;
+      const double m2p = Spp - Sp * Sp / nn;
+      const double com = Sop - So * Sp / nn;
+      float r = __int_as_float(0x7fc00000);
+      if (!ocst && m2o > 0.0 && m2p > 0.0) r = (float)fmin(1.0, fmax(-1.0, com / sqrt(m2o * m2p)));
+      if (tgt_id >= 0) a.rhoT[(size_t)tgt_id * a.ldr + a.lib_col[lib0 + l]] = r;
+      Sp = Spp = Sop = 0.0;
+    }
+  }
+  qglob += ws.total;
+}
+
+__global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(LookupArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  float* tgt = reinterpret_cast<float*>(smem);
+  const size_t tgt_bytes = (size_t)a.T * 128;
+  uint8_t* rings = smem + tgt_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)kLookupWarps * 2 * a.stage_bytes);
+  __shared__ int64_t s_item;
+
+  const int lane = lane_id(), w = warp_id();
+  if (threadIdx.x < kLookupWarps * 2) mbar_init(bars + threadIdx.x, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  uint8_t* ring = rings + (size_t)w * 2 * a.stage_bytes;
+  uint64_t* wbars = bars + 2 * w;
+  uint32_t qglob = 0;
+
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(a.counter, 1);
+    __syncthreads();
+    const int64_t item = s_item;
+    if (item >= a.n_items) break;
+    int g = 0;
+    while (g + 1 < a.ngroups && a.g_item0[g + 1] <= item) ++g;
+    const int64_t rem = item - a.g_item0[g];
+    const int nblk = a.g_nblk[g];
+    const int lsub = (int)(rem / nblk);
+    const int blk = a.g_blk0[g] + (int)(rem - (int64_t)lsub * nblk);
+    const int E = a.g_E[g];
+
+    // stage the 32-target block, time-major
+    {
+      const float4* src = reinterpret_cast<const float4*>(a.Y + (size_t)blk * 32);
+      float4* dst = reinterpret_cast<float4*>(tgt);
+      const int64_t ld4 = a.ldy / 4;
+      for (int v = threadIdx.x; v < a.T * 8; v += blockDim.x) {
+        const int t = v >> 3, c = v & 7;
+        dst[v] = src[(size_t)t * ld4 + c];
+      }
+    }
+    __syncthreads();
+
+    const int per_warp = a.LS / kLookupWarps;
+    const int lib0 = lsub * a.LS + w * per_warp;
+    const int nl = max(0, min(per_warp, a.nlib - lib0));
+    if (nl > 0) {
+      const int k = E + 1;
+      switch (k) {
+#define CMB_K(kk) case kk: warp_libraries<kk>(a, tgt, ring, wbars, qglob, E, lib0, nl, blk * 32); break;
+        CMB_K(2) CMB_K(3) CMB_K(4) CMB_K(5) CMB_K(6) CMB_K(7) CMB_K(8) CMB_K(9) CMB_K(10)
+        CMB_K(11) CMB_K(12) CMB_K(13) CMB_K(14) CMB_K(15) CMB_K(16) CMB_K(17) CMB_K(18) CMB_K(19)
+        CMB_K(20) CMB_K(21) CMB_K(22) CMB_K(23) CMB_K(24) CMB_K(25) CMB_K(26) CMB_K(27) CMB_K(28)
+        CMB_K(29) CMB_K(30) CMB_K(31)
+#undef CMB_K
+        default: break;
+      }
+    }
+    __syncthreads();
+  }
+  (void)lane;
+}
+
+}  // namespace
+
+int lookup_smem_bytes(int T, int stage_bytes) {
+  return T * 128 + kLookupWarps * 2 * stage_bytes + kLookupWarps * 2 * 8;
+}
+
+int lookup_stage_bytes(int T, int max_rec_bytes) {
+  const int budget = 232448 - T * 128 - kLookupWarps * 2 * 8 - 1024;  // 1 KB static reserve
+  int sb = budget / (kLookupWarps * 2);
+  sb = sb - sb % 16;
+  if (sb > 4096) sb = 4096;
+  // at least two records per slot keeps the ring useful
+  if (sb < 2 * max_rec_bytes) return 0;
+  return sb;
+}
+
+cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st) {
+  const int smem = lookup_smem_bytes(a.T, a.stage_bytes);
+  cudaError_t e = cudaFuncSetAttribute(lookup_xmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  lookup_xmap_kernel<<<grid, kLookupWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace cmb

@@ -1,0 +1,91 @@
+"""Multi-GPU xmap: library-row sharding over one process per GPU.
+
+North-star row (e) of SURVEY.md section 8: the dataset X[N][T] is replicated
+once from rank 0 with an NCCL broadcast over NVLink, rank g computes the rho
+columns of libraries [g N / G, (g+1) N / G) for every target with the
+single-device kernels (``cmb_xmap_dev``), and the slabs are gathered to
+rank 0.  There is no other collective: pairs are independent and every rank
+processes the same distinct-E set, so per-rank work is uniform and rho is
+bitwise identical for any G (per-pair arithmetic does not depend on G).
+
+torch.distributed is plumbing only (process group, device buffers, the two
+collectives); all arithmetic runs in libcmb200.
+"""
+
+from __future__ import annotations
+
+from typing import Callable
+
+import numpy as np
+
+from . import _native as nat
+
+
+def shard_bounds(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous library block of ``rank`` (sizes differ by at most one)."""
+    base, extra = divmod(n, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def slab_width(n: int, world: int) -> int:
+    """Common (padded) column count of every rank's rho slab, a multiple of 4."""
+    w = -(-n // world)
+    return (w + 3) // 4 * 4
+
+
+def native_shard(X, estar: np.ndarray, tau: int, lo: int, hi: int, slab, stats: np.ndarray | None,
+                 device: int, stream_handle: int | None) -> None:
+    """rho_T[:, 0:hi-lo] of libraries [lo, hi) into ``slab`` (torch, [N][ldr]) on the device."""
+    N, T = X.shape
+    est = np.ascontiguousarray(estar, dtype=np.int32)
+    nat.call("cmb_xmap_dev", device, X.data_ptr(), N, T, X.stride(0), nat.ptr(est), tau, lo, hi,
+             slab.data_ptr(), slab.stride(0), stream_handle, nat.ptr(stats))
+
+
+def xmap_sharded(X, estar: np.ndarray, tau: int = 1, group=None, compute: Callable | None = None,
+                 stats: np.ndarray | None = None, broadcast: bool = True):
+    """Sharded all-to-all cross map.
+
+    ``X``: torch tensor [N][T] float32 on this rank's device (meaningful on
+    rank 0 when ``broadcast``).  Returns on rank 0 a torch tensor
+    rho_T[N][G * slab] (target-major; column c of rank g's slab is library
+    shard_bounds(N, G, g)[0] + c; padding columns are NaN), None elsewhere.
+    ``compute`` replaces the device kernel (tests run the same plumbing on
+    CPU with gloo and an oracle-backed compute).
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    N = X.shape[0]
+    if world > 1 and broadcast:
+        dist.broadcast(X, src=0, group=group)
+    lo, hi = shard_bounds(N, world, rank)
+    w = slab_width(N, world)
+    slab = torch.full((N, w), float("nan"), dtype=torch.float32, device=X.device)
+    if compute is None:
+        dev = X.device.index or 0
+        handle = torch.cuda.current_stream(X.device).cuda_stream
+        native_shard(X, estar, tau, lo, hi, slab, stats, dev, handle)
+    else:
+        compute(X, estar, tau, lo, hi, slab)
+    if world == 1:
+        return slab
+    gathered = [torch.empty_like(slab) for _ in range(world)] if rank == 0 else None
+    dist.gather(slab, gathered, dst=0, group=group)
+    if rank != 0:
+        return None
+    return torch.cat(gathered, dim=1)
+
+
+def assemble(rhoT_slabs, n: int, world: int) -> np.ndarray:
+    """rho[lib, tgt] (numpy, float32) from the gathered target-major slabs."""
+    rt = rhoT_slabs.cpu().numpy() if hasattr(rhoT_slabs, "cpu") else np.asarray(rhoT_slabs)
+    w = slab_width(n, world)
+    cols = []
+    for g in range(world):
+        lo, hi = shard_bounds(n, world, g)
+        cols.append(rt[:, g * w: g * w + (hi - lo)])
+    return np.concatenate(cols, axis=1).T

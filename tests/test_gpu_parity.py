@@ -1,0 +1,266 @@
+"""GPU parity: the CUDA path (through libcmb200's C ABI) against the oracle and
+the reference's own golden vectors.
+
+Tolerances (north_star): neighbour indices identical (the kNN kernel certifies
+every row in fp64 and re-selects uncertified rows exactly, so no exceptions
+are expected); predictions and rho within 1e-4.  Paths that are fp64 end to
+end (tables, lookup_batch, simplex, edim) are held to much tighter bounds.
+"""
+
+import numpy as np
+import pytest
+
+import crossmap_oracle as O
+import paper_2105_12301_b200 as P
+from paper_2105_12301_b200 import _native
+from conftest import parse_case, parse_edim_case
+
+pytestmark = pytest.mark.gpu
+
+RHO_TOL = 1e-4        # north_star: predictions and rho
+W_TOL_EXACT = 1e-12   # weights from identical fp64 distances (exp() ulp differences only)
+
+
+def _nan(r):
+    return np.nan if r is None else r
+
+
+# ---------------------------------------------------------------- known-answer tests
+def test_distance_kats():
+    assert np.array_equal(P.pairwise_distances([7.0] * 4, P.EmbeddingSpec(1, 1)).values, np.zeros((4, 4)))
+    assert P.pairwise_distances([0.0, 3.0], P.EmbeddingSpec(1, 1)).values.tolist() == [[0.0, 9.0], [9.0, 0.0]]
+    assert P.pairwise_distances([0.0, 1.0, 3.0], P.EmbeddingSpec(2, 1)).values.tolist() == [[0.0, 5.0], [5.0, 0.0]]
+
+
+def test_topk_kats_and_ties():
+    m = np.array([[5.0, 1, 3, 2], [1, 0, 2, 3], [3, 2, 0, 1], [2, 3, 1, 0]])
+    d, i = P.partial_sort_topk(m, 2)
+    assert i[0].tolist() == [1, 3] and d[0].tolist() == [1.0, 2.0]
+    m = np.ones((4, 4)) - np.eye(4)
+    m[0] = [0.0, 1.0, 1.0, 1.0]
+    assert P.partial_sort_topk(m, 2)[1][0].tolist() == [1, 2]
+    rng = np.random.default_rng(0)
+    for trial in range(30):
+        n = int(rng.integers(4, 40))
+        m = rng.integers(0, 4, size=(n, n)).astype(float) if trial % 2 else rng.random((n, n))
+        np.fill_diagonal(m, 0.0)
+        k = int(rng.integers(1, n))
+        d, idx = P.partial_sort_topk(m, k)
+        od, oi = O.select_k(m, k)
+        assert np.array_equal(idx, oi) and np.array_equal(d, od)
+
+
+def test_weight_kats():
+    from test_oracle import WEIGHTS_0_0_4, WEIGHTS_1_4_9
+    assert np.allclose(P.normalize_to_weights(np.array([[1.0, 4.0, 9.0]]))[0], WEIGHTS_1_4_9, atol=1e-12)
+    assert np.allclose(P.normalize_to_weights(np.array([[0.0, 0.0, 4.0]]))[0], WEIGHTS_0_0_4, atol=1e-12)
+    assert np.allclose(P.normalize_to_weights(np.zeros((2, 4))), 0.25, atol=1e-15)
+    with pytest.raises(P.ParameterError):
+        P.normalize_to_weights(np.array([[2.0, 1.0]]))
+
+
+def test_hand_lookup_kat():
+    from test_oracle import HAND_PREDICTIONS, HAND_RHO
+    table = P.NeighborTable(np.array([[1, 2], [0, 2], [0, 1]]), np.array([[0.75, 0.25]] * 3), P.EmbeddingSpec(1, 1))
+    out = P.lookup_batch(table, [np.array([1.0, 2.0, 3.0])], want_predictions=True)[0]
+    assert out.predicted.tolist() == HAND_PREDICTIONS
+    assert abs(out.rho - HAND_RHO) <= 1e-12
+
+
+def test_constant_series_degenerate_table():
+    table = P.build_knn_table(np.full(9, 1.5), P.EmbeddingSpec(1, 1), k=3)
+    assert np.allclose(table.weights, 1 / 3, atol=1e-15)
+    assert table.indices[0].tolist() == [1, 2, 3]
+    assert table.indices[4].tolist() == [0, 1, 2]
+
+
+# ---------------------------------------------------------------- reference goldens
+def test_tables_match_reference_goldens(golden):
+    g = golden("knn_lookup")
+    _native.diagnostics()
+    for key in g["cases"]:
+        E, tau = parse_case(key)
+        t = P.build_knn_table(g[f"{key}_x"], P.EmbeddingSpec(E, tau))
+        assert np.array_equal(t.indices, g[f"{key}_idx"]), key
+        assert np.max(np.abs(t.weights - g[f"{key}_w"])) <= W_TOL_EXACT, key
+        # materialised path agrees too
+        slow = P.oracle_knn(g[f"{key}_x"], P.EmbeddingSpec(E, tau))
+        assert np.array_equal(slow.indices, g[f"{key}_idx"]), key
+    diag = _native.diagnostics()
+    print("kNN diagnostics:", diag)
+
+
+def test_lookup_matches_reference_goldens(golden):
+    g = golden("knn_lookup")
+    for key in g["cases"]:
+        E, tau = parse_case(key)
+        table = P.NeighborTable(g[f"{key}_idx"].astype(np.int64), g[f"{key}_w"], P.EmbeddingSpec(E, tau))
+        outs = P.lookup_batch(table, list(g[f"{key}_targets"]), want_predictions=True)
+        rho = np.array([_nan(o.rho) for o in outs])
+        assert np.array_equal(np.isnan(rho), np.isnan(g[f"{key}_rho"])), key
+        assert np.nanmax(np.abs(rho - g[f"{key}_rho"]), initial=0) <= 1e-12, key
+        assert np.max(np.abs(np.stack([o.predicted for o in outs]) - g[f"{key}_pred"])) <= 1e-12, key
+
+
+def test_edim_and_simplex_match_reference_goldens(golden):
+    g = golden("edim")
+    for key in g["cases"]:
+        E_max, tau, Tp = parse_edim_case(key)
+        x = g[f"{key}_x"]
+        res = P.optimal_embedding(x, e_max=E_max, tau=tau, tp=Tp)
+        curve = np.array([res.rho_by_e[e] for e in range(1, E_max + 1)])
+        assert np.max(np.abs(curve - g[f"{key}_curve"])) <= 1e-10, key
+        assert res.e_star == int(g[f"{key}_estar"]), key
+        s = P.simplex_self_predict(x, P.EmbeddingSpec(3, tau), tp=Tp)
+        assert abs(s - float(g[f"{key}_simplex3"])) <= 1e-10, key
+
+
+def test_config1_pipeline(golden):
+    g = golden("config1")
+    X = g["f32_x"]
+    est, rho_curves = P.edim(X.T, 20, 1, 1)
+    assert est.tolist() == g["f32_estar"].tolist() == [1, 2]
+    assert np.max(np.abs(rho_curves - g["f32_curves"])) <= 1e-10
+    m = P.ccm_matrix(X.T, ["driver", "response"])
+    assert np.max(np.abs(m.skill - g["f32_rho"])) <= RHO_TOL
+    fixed = P.xmap(X.T, [2, 2])
+    assert np.max(np.abs(fixed - g["f32_rho_e22"])) <= RHO_TOL
+    assert fixed[1, 0] - fixed[0, 1] > 0.15  # directionality (test_acceptance.py:150-178)
+
+
+def test_mixed20_pipeline(golden):
+    g = golden("mixed20")
+    X = g["x"]
+    m = P.ccm_matrix(X.T, list(g["names"]))
+    est, curves = P.edim(X.T, 20, 1, 1)
+    assert est.tolist() == g["estar"].tolist()
+    assert np.max(np.abs(curves - g["curves"])) <= 1e-10
+    assert np.array_equal(np.isnan(m.skill), np.isnan(g["rho"]))
+    assert np.nanmax(np.abs(m.skill - g["rho"])) <= RHO_TOL
+
+
+# ---------------------------------------------------------------- oracle equivalence sweeps
+def test_oracle_equivalence_sweep():
+    """>= 100 random instances (test_acceptance.py:44-68): exact indices."""
+    rng = np.random.default_rng(2024)
+    count = 0
+    _native.diagnostics()
+    for rep in range(12):
+        for E in (1, 5, 20):
+            for tau in (1, 2, 3):
+                span = (E - 1) * tau
+                length = int(rng.integers(span + E + 3, 501))
+                if rep % 2 == 0:
+                    x = rng.random(length)
+                else:
+                    x = P.logistic_map(length, seed=int(rng.integers(1 << 30)), r=3.6 + 0.39 * rng.random()).values
+                idx, w = O.knn_table(x, E, tau)
+                t = P.build_knn_table(x, P.EmbeddingSpec(E, tau))
+                assert np.array_equal(t.indices, idx), (E, tau, length)
+                assert np.max(np.abs(t.weights - w)) <= W_TOL_EXACT
+                count += 1
+    assert count >= 100
+    print("diagnostics:", _native.diagnostics())
+
+
+def test_heavy_ties_exact():
+    rng = np.random.default_rng(99)
+    for x in (rng.integers(0, 3, 300).astype(float), np.round(rng.random(400) * 8) / 8,
+              P.logistic_map(120, r=4.0, v0=0.5).values):
+        for E, tau in ((1, 1), (2, 1), (5, 2), (7, 1)):
+            idx, w = O.knn_table(x, E, tau)
+            t = P.build_knn_table(x, P.EmbeddingSpec(E, tau))
+            assert np.array_equal(t.indices, idx)
+            assert np.max(np.abs(t.weights - w)) <= W_TOL_EXACT
+
+
+def test_float64_inputs_not_float32_representable():
+    rng = np.random.default_rng(5)
+    for scale, shift in ((1.0, 0.0), (1e-3, 1000.0)):
+        x = shift + scale * rng.standard_normal(700)
+        for E in (1, 3, 9):
+            idx, w = O.knn_table(x, E, 1)
+            t = P.build_knn_table(x, P.EmbeddingSpec(E, 1))
+            assert np.array_equal(t.indices, idx)
+
+
+def test_xmap_against_oracle_on_mixed_256():
+    X = P.mixed_dataset(256, 1450, seed=2105).astype(np.float64)
+    est, _ = P.edim(X.T, 20, 1, 1)
+    rho = P.xmap(X.T, est)
+    libs = [0, 7, 19, 100, 255]
+    ref, _ = O.xmap(list(X), [int(e) for e in est], 1, libraries=libs)
+    for l in libs:
+        assert np.array_equal(np.isnan(rho[l]), np.isnan(ref[l]))
+        assert np.nanmax(np.abs(rho[l] - ref[l])) <= RHO_TOL, l
+    # determinism
+    again = P.xmap(X.T, est)
+    assert np.array_equal(rho, again, equal_nan=True)
+    # native layout returns the same matrix
+    tm = P.xmap(X.T, est, layout=P.LAYOUT_TGT_MAJOR)
+    assert np.array_equal(rho, tm, equal_nan=True)
+
+
+def test_edim_against_oracle_batch():
+    X = P.mixed_dataset(40, 700, seed=77).astype(np.float64)
+    est, rho = P.edim(X.T, 20, 1, 1)
+    for i in range(0, 40, 3):
+        star, curve = O.edim(X[i], 20, 1, 1)
+        oc = np.array([curve[e] for e in range(1, 21)])
+        assert np.max(np.abs(rho[i] - oc)) <= 1e-10, i
+        assert est[i] == star, (i, est[i], star)
+
+
+def test_xmap_zero_variance_and_permutation():
+    rng = np.random.default_rng(3)
+    X = np.stack([P.logistic_map(400, seed=42, r=3.8).values, np.full(400, 2.0),
+                  P.logistic_map(400, seed=43, r=3.9).values, rng.random(400)])
+    m = P.ccm_pairwise(P.Dataset(tuple(P.TimeSeries(X[i], f"s{i}") for i in range(4))), P.CcmConfig(e_max=4))
+    assert np.all(np.isnan(m.rho[1, :])) and np.all(np.isnan(m.rho[:, 1]))
+    live = np.ix_([0, 2, 3], [0, 2, 3])
+    assert np.all(np.isfinite(m.rho[live]))
+    perm = [2, 0, 3, 1]
+    m2 = P.ccm_pairwise(P.Dataset(tuple(P.TimeSeries(X[i], f"s{i}") for i in perm)), P.CcmConfig(e_max=4))
+    assert np.array_equal(m2.rho, m.rho[np.ix_(perm, perm)], equal_nan=True)
+
+
+def test_lookup_affine_invariance_and_zero_variance():
+    v = P.logistic_map(400, seed=18, r=3.7).values
+    table = P.build_knn_table(v, P.EmbeddingSpec(2, 1))
+    y = P.uniform_noise(400, seed=19).values
+    base = P.lookup_batch(table, [y])[0].rho
+    moved = P.lookup_batch(table, [2.5 * y - 1.0])[0].rho
+    assert abs(base - moved) <= 1e-9
+    assert P.lookup_batch(table, [np.full(400, 2.0)])[0].rho is None
+
+
+def test_pearson_stream_matches_two_pass():
+    rng = np.random.default_rng(21)
+    for _ in range(20):
+        n = int(rng.integers(2, 9000))
+        a = rng.standard_normal(n)
+        b = 0.4 * a + rng.standard_normal(n)
+        da, db = a - a.mean(), b - b.mean()
+        ref = (da * db).sum() / np.sqrt((da ** 2).sum() * (db ** 2).sum())
+        assert abs(P.pearson_stream(a, b) - ref) <= 1e-10
+    with pytest.raises(P.ZeroVarianceError):
+        P.pearson_stream([1.0, 1.0, 1.0], [1.0, 2.0, 3.0])
+
+
+def test_period2_ties_to_smaller_dimension():
+    x = np.tile([0.2, 0.8], 100).astype(float)
+    assert P.optimal_embedding(x, e_max=4).e_star == 1
+
+
+def test_errors_surface_reference_types():
+    with pytest.raises(P.ZeroVarianceError):
+        P.optimal_embedding(np.full(200, 1.0), e_max=3)
+    with pytest.raises(P.SeriesTooShortError):
+        P.optimal_embedding(P.uniform_noise(20, seed=0).values, e_max=20)
+    with pytest.raises(P.ZeroVarianceError):
+        P.simplex_self_predict(np.full(100, 3.0), P.EmbeddingSpec(2, 1), tp=1)
+    with pytest.raises(P.ParameterError, match="samples"):
+        t = P.build_knn_table(P.uniform_noise(50, seed=22).values, P.EmbeddingSpec(2, 1))
+        P.lookup_batch(t, [np.zeros(40)])
+    with pytest.raises(P.SeriesTooShortError):
+        P.build_knn_table(np.arange(5, dtype=float), P.EmbeddingSpec(3, 1))
