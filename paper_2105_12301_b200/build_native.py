@@ -63,7 +63,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     if jobs:
         with ThreadPoolExecutor(max_workers=len(jobs)) as pool:
             logs = list(pool.map(compile_one, jobs))
-        with open(BUILD / "ptxas.log", "a") as fh:
+        with open(BUILD / "ptxas.log", "w") as fh:
             for name, text in logs:
                 fh.write(f"==== {name}\n{text}\n")
                 if verbose:

@@ -152,8 +152,8 @@ static int knn_raw(Ctx* ctx, cudaStream_t st, const double* x_dev, const float* 
   a.need = 1u << (E - 1);
   a.mode = KNN_RAW;
   a.k_raw = k;
-  a.rows_per_block = 64;
-  a.nrb = (int)((len + 63) / 64);
+  a.rows_per_block = 128;
+  a.nrb = (int)((len + 127) / 128);
   a.err_m = err_dev;
   a.raw_idx = idx_dev;
   a.raw_w = w_dev;
@@ -179,7 +179,7 @@ static int edim_core(Ctx* ctx, cudaStream_t st, const float* x32, const double* 
                      const float* err, int64_t N, int64_t len, int64_t ld, int E_hi, uint32_t need,
                      int tau, int Tp, double* rho_dev, int32_t* estar_dev) {
   const int L = (int)(len - Tp);
-  const int rpb = 64;
+  const int rpb = 128;
   const int nrb = (L + rpb - 1) / rpb;
   // batch libraries to bound the partial-moment buffer (~256 MB)
   int64_t batch = std::max<int64_t>(1, (256ll << 20) / ((int64_t)nrb * E_hi * 5 * 8));
@@ -269,10 +269,6 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   CMB_CUDA(launch_fill_nan(rhoT, N, ncols, ldr, st));
   if (la.ngroups == 0 || lib_rows.empty()) return CMB_OK;
   const int stage = lookup_stage_bytes((int)T, max_rec);
-  if (stage == 0) {
-    set_error("series length %lld too long for the shared-memory resident lookup", (long long)T);
-    return CMB_ERR_UNSUPPORTED;
-  }
 
   // ---- device staging
   const int64_t slots = (int64_t)slot_tgt.size();
@@ -325,7 +321,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   cudaEvent_t ev[3];
   for (auto& e : ev) CMB_CUDA(cudaEventCreate(&e));
   float ms_tab = 0, ms_look = 0;
-  const int rpb = 64;
+  const int rpb = 128;
   for (int64_t c0 = 0; c0 < (int64_t)lib_rows.size(); c0 += C) {
     const int64_t nc = std::min<int64_t>(C, (int64_t)lib_rows.size() - c0);
     KnnArgs a;

@@ -37,6 +37,7 @@ struct KnnArgs {
   double* raw_w;
   double* raw_d;
   unsigned long long* diag; // [0] exact fallbacks, [1] rows checked
+  int x64_smem;             // set by the launcher: stage the float64 series in shared memory
 };
 
 int sweep_width(int e_hi);
@@ -75,8 +76,9 @@ struct LookupArgs {
 };
 
 constexpr int kLookupWarps = 16;
-int lookup_smem_bytes(int T, int stage_bytes);
-int lookup_stage_bytes(int T, int max_rec_bytes);  // 0 when T does not fit
+// stage size that selects the non-resident (targets in L2) lookup variant
+constexpr int kNonResidentStage = 4096 + 16;
+int lookup_stage_bytes(int T, int max_rec_bytes);
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st);
 
 // ------------------------------------------------------------------ helpers (utils.cu)

@@ -82,12 +82,15 @@ __device__ __forceinline__ void issue_stage(const WarpStream& ws, int q, uint8_t
   bulk_g2s(slot, src, bytes, bar);
 }
 
-template <int K>
+// RESIDENT: targets staged in shared memory with row stride 32; otherwise
+// gathered from the time-major global array (row stride ldy) through L1/L2.
+template <int K, bool RESIDENT>
 __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float* __restrict__ tgt,
                                                uint8_t* ring, uint64_t* bars, uint32_t& qglob,
                                                int E, int lib0, int nl, int slot_base) {
   constexpr int KP4 = rec_kp4(K), KP8 = rec_kp8(K);
   constexpr int R = 4 * KP4 + 2 * KP8;
+  const int64_t stride = RESIDENT ? 32 : a.ldy;
   const int lane = lane_id();
   const int n = a.T - (E - 1) * a.tau;
   const int off = (E - 1) * a.tau;
@@ -139,12 +142,12 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
         const uint4 v = reinterpret_cast<const uint4*>(rec + 4 * KP4)[c];
         rv[4 * c] = v.x; rv[4 * c + 1] = v.y; rv[4 * c + 2] = v.z; rv[4 * c + 3] = v.w;
       }
-      const float o = tcol[(off + r0 + r) * 32];
+      const float o = tcol[(int64_t)(off + r0 + r) * stride];
       float p = 0.f;
 #pragma unroll
       for (int kk = 0; kk < K; ++kk) {
         const uint32_t row = (rv[kk >> 1] >> (16 * (kk & 1))) & 0xffffu;
-        p = __fmaf_rn(wv[kk], tcol[row * 32], p);
+        p = __fmaf_rn(wv[kk], tcol[(int64_t)row * stride], p);
       }
       sp += p;
       spp = __fmaf_rn(p, p, spp);
@@ -170,10 +173,11 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
   qglob += ws.total;
 }
 
+template <bool RESIDENT>
 __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(LookupArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   float* tgt = reinterpret_cast<float*>(smem);
-  const size_t tgt_bytes = (size_t)a.T * 128;
+  const size_t tgt_bytes = RESIDENT ? (size_t)a.T * 128 : 0;
   uint8_t* rings = smem + tgt_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)kLookupWarps * 2 * a.stage_bytes);
   __shared__ int64_t s_item;
@@ -201,7 +205,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
     const int E = a.g_E[g];
 
     // stage the 32-target block, time-major
-    {
+    if (RESIDENT) {
       const float4* src = reinterpret_cast<const float4*>(a.Y + (size_t)blk * 32);
       float4* dst = reinterpret_cast<float4*>(tgt);
       const int64_t ld4 = a.ldy / 4;
@@ -218,7 +222,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
     if (nl > 0) {
       const int k = E + 1;
       switch (k) {
-#define CMB_K(kk) case kk: warp_libraries<kk>(a, tgt, ring, wbars, qglob, E, lib0, nl, blk * 32); break;
+#define CMB_K(kk) case kk: warp_libraries<kk, RESIDENT>(a, RESIDENT ? tgt : a.Y + (size_t)blk * 32, ring, wbars, qglob, E, lib0, nl, blk * 32); break;
         CMB_K(2) CMB_K(3) CMB_K(4) CMB_K(5) CMB_K(6) CMB_K(7) CMB_K(8) CMB_K(9) CMB_K(10)
         CMB_K(11) CMB_K(12) CMB_K(13) CMB_K(14) CMB_K(15) CMB_K(16) CMB_K(17) CMB_K(18) CMB_K(19)
         CMB_K(20) CMB_K(21) CMB_K(22) CMB_K(23) CMB_K(24) CMB_K(25) CMB_K(26) CMB_K(27) CMB_K(28)
@@ -234,26 +238,25 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
 
 }  // namespace
 
-int lookup_smem_bytes(int T, int stage_bytes) {
-  return T * 128 + kLookupWarps * 2 * stage_bytes + kLookupWarps * 2 * 8;
-}
-
 int lookup_stage_bytes(int T, int max_rec_bytes) {
   const int budget = 232448 - T * 128 - kLookupWarps * 2 * 8 - 1024;  // 1 KB static reserve
   int sb = budget / (kLookupWarps * 2);
   sb = sb - sb % 16;
   if (sb > 4096) sb = 4096;
-  // at least two records per slot keeps the ring useful
-  if (sb < 2 * max_rec_bytes) return 0;
+  // resident targets need room for at least two records per slot; otherwise
+  // the kernel gathers targets from L2 with 4 KB staging slots
+  if (sb < 2 * max_rec_bytes) return kNonResidentStage;
   return sb;
 }
 
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st) {
-  const int smem = lookup_smem_bytes(a.T, a.stage_bytes);
-  cudaError_t e = cudaFuncSetAttribute(lookup_xmap_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const bool resident = a.stage_bytes != kNonResidentStage;
+  const int smem = (resident ? a.T * 128 : 0) + kLookupWarps * 2 * a.stage_bytes + kLookupWarps * 2 * 8;
+  auto kern = resident ? lookup_xmap_kernel<true> : lookup_xmap_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   count_launch();
-  lookup_xmap_kernel<<<grid, kLookupWarps * 32, smem, st>>>(a);
+  kern<<<grid, kLookupWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@ COUPLINGS = (0.25, 0.35, 0.5)
 SINE_PERIODS = (47.0, 131.0)
 BLOCK = 20  # series per tile of the mix
 BLOCK_SEED_STRIDE = 1000
+DIVERGE_STRIDE = 1_000_003
 
 
 def _length(n) -> int:
@@ -59,20 +60,22 @@ def logistic_map(length: int, seed: int | None = None, r: float = 3.8, v0: float
     return TimeSeries(_logistic_iter(np.array([v0]), np.array([float(r)]), length)[0], name)
 
 
-def _coupled_iter(d0, y0, beta, length, r_d=3.8, r_y=3.5, burn_in=200):
+def _coupled_iter(d0, y0, beta, length, r_d=3.8, r_y=3.5, burn_in=200, strict=True):
     d = np.asarray(d0, dtype=np.float64).copy()
     y = np.asarray(y0, dtype=np.float64).copy()
     beta = np.asarray(beta, dtype=np.float64)
     drv = np.empty((d.size, length))
     rsp = np.empty((d.size, length))
-    for t in range(-burn_in, length):
-        if t >= 0:
-            drv[:, t] = d
-            rsp[:, t] = y
-        d, y = r_d * d * (1.0 - d), y * (r_y - r_y * y - beta * d)
-    if not (np.all(np.isfinite(drv)) and np.all(np.isfinite(rsp))):
+    with np.errstate(over="ignore", invalid="ignore"):
+        for t in range(-burn_in, length):
+            if t >= 0:
+                drv[:, t] = d
+                rsp[:, t] = y
+            d, y = r_d * d * (1.0 - d), y * (r_y - r_y * y - beta * d)
+    ok = np.all(np.isfinite(drv), axis=1) & np.all(np.isfinite(rsp), axis=1) & np.isfinite(y)
+    if strict and not ok.all():
         raise ParameterError("coupled map diverged")
-    return drv, rsp
+    return drv, rsp, ok
 
 
 def coupled_logistic(length: int, seed: int, beta: float = 0.4, r_driver: float = 3.8,
@@ -83,7 +86,7 @@ def coupled_logistic(length: int, seed: int, beta: float = 0.4, r_driver: float 
     rng = np.random.default_rng(seed)
     d0 = rng.uniform(0.1, 0.9)
     y0 = rng.uniform(0.1, 0.9)
-    drv, rsp = _coupled_iter([d0], [y0], [beta], length, r_driver, r_response, burn_in)
+    drv, rsp, _ = _coupled_iter([d0], [y0], [beta], length, r_driver, r_response, burn_in)
     return Dataset((TimeSeries(drv[0], "driver"), TimeSeries(rsp[0], "response")))
 
 
@@ -114,7 +117,19 @@ def mixed_dataset(n_series: int, length: int, seed: int = 2105, dtype=np.float32
     init = np.array([[np.random.default_rng(int(s) + 50 + q).uniform(0.1, 0.9, size=2) for q in range(3)]
                      for s in seeds])  # (nb, 3, 2)
     beta = np.broadcast_to(np.array(COUPLINGS), (nb, 3))
-    drv, rsp = _coupled_iter(init[..., 0].ravel(), init[..., 1].ravel(), beta.ravel(), L)
+    drv, rsp, ok = _coupled_iter(init[..., 0].ravel(), init[..., 1].ravel(), beta.ravel(), L,
+                                 strict=False)
+    # A seed whose pair diverges (the reference raises, synthetic.py:92-97) is
+    # replaced by seed + DIVERGE_STRIDE * attempt until the pair stays finite.
+    for flat in np.flatnonzero(~ok):
+        b, q = divmod(int(flat), 3)
+        for attempt in range(1, 100):
+            rng = np.random.default_rng(int(seeds[b]) + 50 + q + DIVERGE_STRIDE * attempt)
+            d0, y0 = rng.uniform(0.1, 0.9), rng.uniform(0.1, 0.9)
+            dd, rr, good = _coupled_iter([d0], [y0], [COUPLINGS[q]], L, strict=False)
+            if good[0]:
+                drv[flat], rsp[flat] = dd[0], rr[0]
+                break
     drv = drv.reshape(nb, 3, L)
     rsp = rsp.reshape(nb, 3, L)
     for q in range(3):

@@ -1,0 +1,71 @@
+"""Multi-process (gloo, world size 2) checks of the library-row sharding plumbing.
+
+The device kernel is replaced by an oracle-backed compute for the CPU run;
+broadcast, shard bounds, slab layout, gather and assembly are the production
+code paths of paper_2105_12301_b200.distributed.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2105_12301_b200.distributed import assemble, shard_bounds, slab_width, xmap_sharded
+
+
+def test_shard_bounds_partition():
+    for n in (1, 7, 8, 53053, 100):
+        for g in (1, 2, 3, 8):
+            spans = [shard_bounds(n, g, r) for r in range(g)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            sizes = [hi - lo for lo, hi in spans]
+            assert max(sizes) - min(sizes) <= 1
+            assert slab_width(n, g) >= max(sizes) and slab_width(n, g) % 4 == 0
+
+
+def _oracle_compute(X, estar, tau, lo, hi, slab):
+    import crossmap_oracle as O
+    series = [X[i].double().numpy() for i in range(X.shape[0])]
+    rho, _ = O.xmap(series, [int(e) for e in estar], tau, workers=1, libraries=list(range(lo, hi)))
+    slab[:, : hi - lo] = torch.from_numpy(rho[lo:hi].T.astype(np.float32))
+
+
+def _worker(rank, world, port, X, estar, out):
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "oracle"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    Xl = X.clone() if rank == 0 else torch.zeros_like(X)
+    res = xmap_sharded(Xl, estar, 1, compute=_oracle_compute)
+    if rank == 0:
+        out.copy_(torch.from_numpy(assemble(res, X.shape[0], world)))
+    else:
+        assert res is None
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("world", [2])
+def test_sharded_xmap_matches_single_process(world):
+    import crossmap_oracle as O
+    from paper_2105_12301_b200.synthetic import mixed_dataset
+    X = torch.from_numpy(mixed_dataset(7, 150, seed=11))
+    estar = np.array([1, 2, 2, 3, 1, 0, 2], dtype=np.int32)
+    out = torch.full((7, 7), float("nan"))
+    out.share_memory_()
+    mp.spawn(_worker, args=(world, _free_port(), X, estar, out), nprocs=world, join=True)
+    ref, _ = O.xmap([X[i].double().numpy() for i in range(7)], estar.tolist(), 1, workers=1)
+    assert np.allclose(out.numpy(), ref.astype(np.float32), equal_nan=True, atol=0)
+    assert np.all(np.isnan(out.numpy()[5, :])) and np.all(np.isnan(out.numpy()[:, 5]))
