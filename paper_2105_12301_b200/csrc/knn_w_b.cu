@@ -1,0 +1,13 @@
+// Width instantiations of the K1/K2 kernel (split for parallel compilation).
+#include "knn_sweep.cuh"
+
+namespace cmb {
+namespace knn_detail {
+template cudaError_t launch_w<9>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_w<10>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_w<11>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_w<12>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_w<13>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_w<14>(const KnnArgs&, int, cudaStream_t);
+}  // namespace knn_detail
+}  // namespace cmb

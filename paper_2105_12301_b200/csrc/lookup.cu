@@ -63,6 +63,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// shared-memory load at a 32-bit shared address (targets are written only
+// before the __syncthreads that opens a work item, so no memory clobber)
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ void lds_v2(uint32_t addr, float& x, float& y) {
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x), "=f"(y) : "r"(addr));
+}
+__device__ __forceinline__ void lds_v2(uint32_t addr, uint32_t& x, uint32_t& y) {
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(x), "=r"(y) : "r"(addr));
+}
+
 struct WarpStream {
   const uint8_t* base;  // table of the warp's first library
   int n;                // records per library
@@ -108,6 +123,7 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
   const double So = a.obs_s[slot], Soo = a.obs_ss[slot];
   const bool ocst = a.obs_const[slot] != 0;
   const float* __restrict__ tcol = tgt + lane;
+  const uint32_t tbase = RESIDENT ? smem_u32(tcol) : 0u;
 
   // prologue: two stages in flight
   if (lane == 0) {
@@ -123,31 +139,38 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
     const uint32_t g = qglob + q;
     uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
     mbar_wait(bars + (g & 1), (g >> 1) & 1);
+    const uint32_t slot_s = smem_u32(slotp);
     const int l = q / ws.nst, s = q - l * ws.nst;
     const int r0 = s * ws.RS;
     const int nrec = min(ws.RS, n - r0);
     float sp = 0.f, spp = 0.f, sop = 0.f;
 #pragma unroll 2
     for (int r = 0; r < nrec; ++r) {
-      const uint8_t* rec = slotp + r * R;
-      float wv[KP4];
-      uint32_t rv[KP8 / 2];
+      const uint32_t rec = slot_s + r * R;
+      // broadcast reads as 8-byte loads (one shared wavefront each; a
+      // broadcast 16-byte load costs two, so keep the compiler from merging)
+      float wv[2 * ((K + 1) / 2)];
+      uint32_t rv[2 * ((K + 3) / 4)];
 #pragma unroll
-      for (int c = 0; c < KP4 / 4; ++c) {
-        const float4 v = reinterpret_cast<const float4*>(rec)[c];
-        wv[4 * c] = v.x; wv[4 * c + 1] = v.y; wv[4 * c + 2] = v.z; wv[4 * c + 3] = v.w;
-      }
+      for (int c = 0; c < (K + 1) / 2; ++c) lds_v2(rec + 8 * c, wv[2 * c], wv[2 * c + 1]);
 #pragma unroll
-      for (int c = 0; c < KP8 / 8; ++c) {
-        const uint4 v = reinterpret_cast<const uint4*>(rec + 4 * KP4)[c];
-        rv[4 * c] = v.x; rv[4 * c + 1] = v.y; rv[4 * c + 2] = v.z; rv[4 * c + 3] = v.w;
-      }
-      const float o = tcol[(int64_t)(off + r0 + r) * stride];
-      float p = 0.f;
+      for (int c = 0; c < (K + 3) / 4; ++c) lds_v2(rec + 4 * KP4 + 8 * c, rv[2 * c], rv[2 * c + 1]);
+      float o, p = 0.f;
+      if (RESIDENT) {
+        // 32-bit shared addresses: byte offset of sample row s is s << 7
+        o = lds_f32(tbase + ((uint32_t)(off + r0 + r) << 7));
 #pragma unroll
-      for (int kk = 0; kk < K; ++kk) {
-        const uint32_t row = (rv[kk >> 1] >> (16 * (kk & 1))) & 0xffffu;
-        p = __fmaf_rn(wv[kk], tcol[(int64_t)row * stride], p);
+        for (int kk = 0; kk < K; ++kk) {
+          const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+          p = __fmaf_rn(wv[kk], lds_f32(tbase + (row << 7)), p);
+        }
+      } else {
+        o = tcol[(int64_t)(off + r0 + r) * stride];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+          p = __fmaf_rn(wv[kk], tcol[(int64_t)row * stride], p);
+        }
       }
       sp += p;
       spp = __fmaf_rn(p, p, spp);
