@@ -415,6 +415,7 @@ int cmb_diagnostics(int dev, int64_t* out, int n) {
   CMB_CUDA(cudaMemcpyAsync(h, ctx->buf[B_DIAG].p, sizeof(h), cudaMemcpyDeviceToHost, st));
   CMB_CUDA(cudaMemsetAsync(ctx->buf[B_DIAG].p, 0, sizeof(h), st));
   CMB_CUDA(cudaStreamSynchronize(st));
+  h[7] = h[2];
   h[2] = (unsigned long long)g_launches.exchange(0);
   for (int q = 0; q < n && q < 8; ++q) out[q] = (int64_t)h[q];
   return CMB_OK;

@@ -29,7 +29,9 @@ cudaError_t launch_knn_sweep(const KnnArgs& a_in, cudaStream_t st) {
   if (W < 0) return cudaErrorInvalidValue;
   const int grid = a.nlib * a.nrb;
   if (grid == 0) return cudaSuccess;
-  a.x64_smem = (a.L + a.Tp) <= 6144 ? 1 : 0;
+  // float64 samples feed the exact re-rank (rare in TABLE mode: read them from L1/L2
+  // there and keep shared memory for a third CTA per SM) and every EDIM/RAW row
+  a.x64_smem = (a.mode != KNN_TABLE && (a.L + a.Tp) <= 6144) ? 1 : 0;
   switch (W) {
 #define CMB_W(n) case n: return launch_w<n>(a, grid, st);
     CMB_W(1) CMB_W(2) CMB_W(3) CMB_W(4) CMB_W(5) CMB_W(6) CMB_W(7) CMB_W(8) CMB_W(9) CMB_W(10)

@@ -47,7 +47,7 @@ namespace knn_detail {
 #define kInfF __int_as_float(0x7f800000)
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kCand = 4;                 // candidates per lane per sweep step (absorb_hits assumes 4)
+constexpr int kCand = 4;                 // candidates per lane per sweep step
 constexpr int kStep = 32 * kCand;        // candidates per warp per sweep step
 constexpr int kNoJ = 0x7fffffff;
 
@@ -212,6 +212,7 @@ static __device__ __noinline__ int compact_lists(Entry* L, Entry* B, int lc, int
 struct RowCtx {
   int i, L, tau, mode, k_raw;
   uint32_t act;
+  unsigned long long* diag;  // [3] hits appended, [4] compactions, [5] hit events
 };
 
 __device__ __forceinline__ int k_of(int mode, int k_raw, int e) { return mode == KNN_RAW ? k_raw : e + 2; }
@@ -222,38 +223,17 @@ __device__ __forceinline__ Entry* list_of(Entry* wl, int mode, int e) {
   return wl + (mode == KNN_RAW ? 0 : list_off(e));
 }
 
-// Append this step's hits of dimension index e to its buffer (out of line:
-// keeps the sweep loop small in the instruction cache).  Invalid candidates
-// arrive with d = +inf.  Updates the shared threshold and counts.
-static __device__ __noinline__ void absorb_hits(Entry* Le, Entry* Be, int* cnt, float* thr_slot,
-                                                int Kp, float d0, float d1, float d2, float d3,
-                                                int jc) {
-  const int lane = lane_id();
-  int lc = cnt[0], bc = cnt[1];
+// Merge the hit buffer into the list and tighten the shared threshold (out of
+// line: rare, and keeps the sweep loop small in the instruction cache).
+static __device__ __noinline__ void compact_into(Entry* Le, Entry* Be, int* cnt, float* thr_slot,
+                                                 int Kp) {
+  const int lc = compact_lists(Le, Be, cnt[0], cnt[1], Kp);
   float t = *thr_slot;
-#pragma unroll 1
-  for (int q = 0; q < kCand; ++q) {
-    const float dq = q == 0 ? d0 : q == 1 ? d1 : q == 2 ? d2 : d3;
-    unsigned m = __ballot_sync(CMB_FULL, dq < t);
-    if (!m) continue;
-    if (bc + __popc(m) > kCap) {
-      lc = compact_lists(Le, Be, lc, bc, Kp);
-      bc = 0;
-      if (lc == Kp) t = fminf(t, Le[Kp - 1].d);
-      m = __ballot_sync(CMB_FULL, dq < t);
-    }
-    if ((m >> lane) & 1u) {
-      Entry h;
-      h.d = dq;
-      h.j = jc + 32 * q + lane;
-      Be[bc + __popc(m & ((1u << lane) - 1u))] = h;
-    }
-    bc += __popc(m);
-  }
+  if (lc == Kp) t = fminf(t, Le[Kp - 1].d);
   __syncwarp();
-  if (lane == 0) {
+  if (lane_id() == 0) {
     cnt[0] = lc;
-    cnt[1] = bc;
+    cnt[1] = 0;
     *thr_slot = t;
   }
   __syncwarp();
@@ -262,15 +242,22 @@ static __device__ __noinline__ void absorb_hits(Entry* Le, Entry* Be, int* cnt, 
 // One sweep step: kCand x 32 consecutive candidates, every swept dimension.
 // Runtime loop over e (xi and thresholds are warp-uniform shared values), so
 // the hot loop stays a few hundred bytes of code.  TAIL: candidates may run
-// past n_E of the active dimensions and need per-dimension masking.
+// past n_E of the active dimensions and need per-dimension masking.  Hits are
+// appended to the dimension's buffer; a buffer holding Kp candidates while
+// the list is still empty, or half full, is compacted so the threshold becomes
+// exact early.
 template <bool TAIL>
 __device__ __forceinline__ void sweep_step(const float* __restrict__ xs, int jc, const RowCtx& r,
                                            int eh, const float* __restrict__ xi_w,
                                            float* thr_w, Entry* wl, Entry* wb, int* wc) {
   const int lane = lane_id();
+  const unsigned below = (1u << lane) - 1u;
   float d[kCand];
 #pragma unroll
-  for (int q = 0; q < kCand; ++q) d[q] = (jc + 32 * q + lane == r.i) ? kInfF : 0.f;  // self excluded
+  for (int q = 0; q < kCand; ++q) {
+    const int j = jc + 32 * q + lane;
+    d[q] = (j == r.i || j >= r.L) ? kInfF : 0.f;  // self and past-the-end excluded
+  }
   const float* xj = xs + jc + lane;
 #pragma unroll 1
   for (int e = 0; e < eh; ++e, xj += r.tau) {
@@ -287,10 +274,41 @@ __device__ __forceinline__ void sweep_step(const float* __restrict__ xs, int jc,
         dm[q] = d[q];
         if (TAIL && jc + 32 * q + lane >= r.L - e * r.tau) dm[q] = kInfF;
       }
+      float t = thr_w[e];
       const float mn = fminf(fminf(dm[0], dm[1]), fminf(dm[2], dm[3]));
-      if (__any_sync(CMB_FULL, mn < thr_w[e]))
-        absorb_hits(list_of(wl, r.mode, e), wb + e * kCap, wc + 2 * e, thr_w + e,
-                    kp_of(r.mode, r.k_raw, r.L, r.tau, e), dm[0], dm[1], dm[2], dm[3], jc);
+      if (__any_sync(CMB_FULL, mn < t)) {
+        int* c = wc + 2 * e;
+        Entry* Be = wb + e * kCap;
+        Entry* Le = list_of(wl, r.mode, e);
+        const int Kp = kp_of(r.mode, r.k_raw, r.L, r.tau, e);
+        int bc = c[1];
+#pragma unroll
+        for (int q = 0; q < kCand; ++q) {
+          unsigned m = __ballot_sync(CMB_FULL, dm[q] < t);
+          if (m) {
+            if (bc + __popc(m) > kCap) {
+              __syncwarp();
+              if (lane == 0) c[1] = bc;
+              __syncwarp();
+              compact_into(Le, Be, c, thr_w + e, Kp);
+              bc = 0;
+              t = thr_w[e];
+              m = __ballot_sync(CMB_FULL, dm[q] < t);
+            }
+            if ((m >> lane) & 1u) {
+              Entry h;
+              h.d = dm[q];
+              h.j = jc + 32 * q + lane;
+              Be[bc + __popc(m & below)] = h;
+            }
+            bc += __popc(m);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) c[1] = bc;
+        __syncwarp();
+        if (bc >= Kp && (c[0] == 0 || 2 * bc >= kCap)) compact_into(Le, Be, c, thr_w + e, Kp);
+      }
     }
   }
 }
@@ -351,6 +369,90 @@ static __device__ __noinline__ void finish_list(Entry* Le, Entry* Be, int* cnt, 
 struct PredObs {
   double p, o;
 };
+
+// Lane-parallel end of row: lane e merges dimension e's hit buffer into its
+// list (sequential insertion by (distance, index)) and, in TABLE mode, when the
+// fp32 top-k set certifies, computes the fp32 weights and writes the record.
+// One lane per dimension keeps all 32 lanes busy instead of k of them.
+// Returns the mask of dimensions that still need the warp fp64 path.
+template <int E_HI>
+static __device__ __noinline__ unsigned lane_finish(const KnnArgs* __restrict__ ap, Entry* wl,
+                                                    Entry* wb, int* wc, int lib, int i,
+                                                    uint32_t act, double M, bool emit) {
+  const KnnArgs& a = *ap;
+  const int lane = lane_id();
+  const int e = lane;
+  bool pending = false;
+  if (e < E_HI && ((act >> e) & 1u)) {
+    Entry* Le = list_of(wl, a.mode, e);
+    const Entry* Be = wb + e * kCap;
+    int* c = wc + 2 * e;
+    const int Kp = kp_of(a.mode, a.k_raw, a.L, a.tau, e);
+    int lc = c[0];
+    const int bc = c[1];
+    for (int b = 0; b < bc; ++b) {
+      const Entry x = Be[b];
+      const unsigned long long key = pack_key(x.d, x.j);
+      int pos;
+      if (lc == Kp) {
+        if (key >= pack_key(Le[Kp - 1].d, Le[Kp - 1].j)) continue;
+        pos = Kp - 1;
+      } else {
+        pos = lc++;
+      }
+      while (pos > 0) {
+        const Entry y = Le[pos - 1];
+        if (pack_key(y.d, y.j) < key) break;
+        Le[pos] = y;
+        --pos;
+      }
+      Le[pos] = x;
+    }
+    c[0] = lc;
+    c[1] = 0;
+    if (emit) {
+      pending = true;
+      if (a.mode == KNN_TABLE) {
+        const int E = e + 1;
+        const int nE = a.L - e * a.tau;
+        const int k = k_of(a.mode, a.k_raw, e);
+        const float dk1 = Le[k - 1].d;
+        const float dk = Le[min(k, Kp - 1)].d;
+        bool ok = (Kp == nE - 1) || (M == 0.0 && dk == 0.f);
+        if (!ok && isfinite(dk) && dk > 1e-30f) {
+          const double A = dk1, B = dk;
+          ok = A + sweep_err_bound(A, E, M) < B - sweep_err_bound(B, E, M);
+        }
+        if (ok) {
+          float scale = sqrtf(Le[0].d);
+          if (scale == 0.f) {
+            scale = 1.f;
+            for (int q = 1; q < k; ++q) {
+              const float dq = sqrtf(Le[q].d);
+              if (dq > 0.f) { scale = dq; break; }
+            }
+          }
+          float tot = 0.f;
+          for (int q = 0; q < k; ++q) tot += fmaxf(expf(-__fdividef(sqrtf(Le[q].d), scale)), FLT_MIN);
+          const int kp4 = rec_kp4(k), kp8 = rec_kp8(k);
+          uint8_t* rec = a.tab[E] + ((size_t)lib * nE + i) * (size_t)rec_bytes(k);
+          float* wr = reinterpret_cast<float*>(rec);
+          uint16_t* rr = reinterpret_cast<uint16_t*>(rec + 4 * kp4);
+          for (int q = 0; q < kp4; ++q)
+            wr[q] = (q < k) ? __fdividef(fmaxf(expf(-__fdividef(sqrtf(Le[q].d), scale)), FLT_MIN), tot) : 0.f;
+          for (int q = 0; q < kp8; ++q) rr[q] = (q < k) ? (uint16_t)(Le[q].j + e * a.tau) : (uint16_t)0;
+          pending = false;
+        }
+      }
+    }
+  }
+  const unsigned need = __ballot_sync(CMB_FULL, pending);
+  if (a.diag) {
+    const unsigned done = __ballot_sync(CMB_FULL, emit && e < E_HI && ((act >> e) & 1u) && !pending);
+    if (lane == 0 && done) atomicAdd(a.diag + 1, (unsigned long long)__popc(done));
+  }
+  return need;
+}
 
 // Per-(row, E) epilogue: certification, weights, emission.  Returns the EDIM
 // prediction and observation (shifted), zeros otherwise.
@@ -548,9 +650,12 @@ knn_sweep_kernel(const __grid_constant__ KnnArgs a) {
   r.tau = tau;
   r.mode = a.mode;
   r.k_raw = a.k_raw;
+  r.diag = a.diag;
   uint32_t prev_act = 0;
 
-  for (int i = r0; i < r1; ++i) {
+  // rows r0 - 1 (warm-up, not emitted: seeds the thresholds of row r0) .. r1 - 1
+  for (int i = max(0, r0 - 1); i < r1; ++i) {
+    const bool emit = i >= r0;
     r.i = i;
     uint32_t act = 0;
     for (int e = 0; e < e_hi; ++e)
@@ -571,21 +676,25 @@ knn_sweep_kernel(const __grid_constant__ KnnArgs a) {
     if (lane < eh) xi_s[w][lane] = xs[i + lane * tau];
     __syncwarp();
 
-    // ---- fp32 sweep over all candidates
+    // ---- fp32 sweep over all candidates, one register-resident chunk at a time
     const int nmin = L - (eh - 1) * tau;
-    for (int jc = 0; jc < L; jc += kStep) {
-      if (jc + kStep > nmin)
-        sweep_step<true>(xs, jc, r, eh, xi_s[w], thr_s[w], wl, wb, wc);
+    for (int c0 = 0; c0 < L; c0 += kStep) {
+      if (c0 + kStep > nmin)
+        sweep_step<true>(xs, c0, r, eh, xi_s[w], thr_s[w], wl, wb, wc);
       else
-        sweep_step<false>(xs, jc, r, eh, xi_s[w], thr_s[w], wl, wb, wc);
+        sweep_step<false>(xs, c0, r, eh, xi_s[w], thr_s[w], wl, wb, wc);
     }
     __syncwarp();
 
-    // ---- per-E: final merge of the hit buffer, then the epilogue (runtime loop)
+    // ---- end of row: lane-parallel merge (+ fp32 TABLE records), then the warp
+    //      fp64 path for the dimensions that need it
+    __syncwarp();
+    unsigned need = lane_finish<E_HI>(&a, wl, wb, wc, lib, i, act, M, emit);
+    __syncwarp();
 #pragma unroll 1
-    for (int e = 0; e < eh; ++e) {
-      if (!((act >> e) & 1u)) continue;
-      finish_list(list_of(wl, r.mode, e), wb + e * kCap, wc + 2 * e, kp_of(r.mode, r.k_raw, L, tau, e));
+    while (need) {
+      const int e = __ffs(need) - 1;
+      need &= need - 1;
       const PredObs po = epilogue_e<E_HI>(&a, list_of(wl, r.mode, e), lib, i, e, xp, M, shift);
       if (a.mode == KNN_EDIM && lane == e) {
         acc0 += po.o;
