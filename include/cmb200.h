@@ -116,16 +116,19 @@ int cmb_edim_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld
 
 /* ---- convergence sweep (no reference implementation) ------- */
 
-/* For each library size sizes[s] and sample q: neighbours restricted to the
- * sampled library points lib_pts[s][q][0..sizes[s]) (sorted point indices,
- * offsets into lib_pts given by lib_off[s]), prediction of every embedded
- * point of every target, Pearson skill.  Series X[N][len]; pairs
- * (lib_ids[p], tgt_ids[p]) at dimension E_pair[p].
+/* Library-size convergence sweep at one embedding dimension E (semantics of
+ * oracle/crossmap_oracle.py: ccm_convergence; parity unpinned -- the
+ * reference has none).  Series X[N][len]; pairs (lib_ids[p], tgt_ids[p]).
+ * For library size sizes[s] (E + 2 <= sizes[s] <= n_E) and sample q, the
+ * sorted embedded-point indices pts[off_s + q*sizes[s] ..] (off_s = sum of
+ * samples * sizes[s'] over s' < s) form the library: every embedded point is
+ * matched to its E + 1 nearest sampled points (self excluded), every target
+ * predicted at every point (Tp = 0), skill by Pearson.
  * rho_out[P][n_sizes][samples] (NaN undefined).                             */
-int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int tau,
-                        const int32_t* lib_ids, const int32_t* tgt_ids, const int32_t* E_pair,
-                        int64_t P, const int32_t* sizes, int n_sizes, int samples,
-                        const int32_t* lib_pts, const int64_t* lib_off, double* rho_out);
+int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E, int tau,
+                        const int32_t* lib_ids, const int32_t* tgt_ids, int64_t P,
+                        const int32_t* sizes, int n_sizes, int samples, const int32_t* pts,
+                        double* rho_out);
 
 #ifdef __cplusplus
 }

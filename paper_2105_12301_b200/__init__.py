@@ -52,18 +52,16 @@ def edim(values, E_max: int = DEFAULT_E_MAX, tau: int = 1, Tp: int = 1):
     return est, rho
 
 
-def ccm(*args, **kwargs):
-    """kEDM ``ccm``: library-size convergence sweep (see convergence.py)."""
-    from .convergence import ccm as _ccm
-    return _ccm(*args, **kwargs)
+from . import convergence  # noqa: E402
+from .convergence import Convergence, ccm, ccm_sweep  # noqa: E402  (kEDM ``ccm``)
 
 
 __all__ = [
-    "CcmConfig", "CcmMatrix", "CcmStats", "CrossmapError", "CsvFormatError", "DEFAULT_E_MAX",
+    "CcmConfig", "CcmMatrix", "CcmStats", "Convergence", "CrossmapError", "CsvFormatError", "DEFAULT_E_MAX",
     "Dataset", "DeviceError", "DistanceMatrix", "EmbeddingSearch", "EmbeddingSpec",
     "LAYOUT_LIB_MAJOR", "LAYOUT_TGT_MAJOR", "NeighborTable", "OptimalEmbedding", "ParameterError",
     "PearsonAggregate", "PredictionOutput", "SeriesTooShortError", "SkillMatrix", "TimeSeries",
-    "ZeroVarianceError", "as_values", "build_knn_table", "ccm", "ccm_matrix", "ccm_pairwise",
+    "ZeroVarianceError", "as_values", "build_knn_table", "ccm", "ccm_matrix", "ccm_pairwise", "ccm_sweep",
     "coupled_logistic", "edim", "embedded_point", "gen_synthetic", "group_by_optimal_e",
     "logistic_map", "lookup_batch", "mixed_dataset", "normalize_to_weights", "optimal_embedding",
     "oracle_knn", "pairwise_distances", "partial_sort_topk", "pearson_stream", "simplex",

@@ -44,8 +44,8 @@ _SIGNATURES = {
                      C.c_int),
     "cmb_edim_dev": ([C.c_int, _P, _i64, _i64, _i64, C.c_int, C.c_int, C.c_int, _P, _P, _P],
                      C.c_int),
-    "cmb_ccm_convergence": ([C.c_int, _P, _i64, _i64, C.c_int, _P, _P, _P, _i64, _P, C.c_int,
-                             C.c_int, _P, _P, _P], C.c_int),
+    "cmb_ccm_convergence": ([C.c_int, _P, _i64, _i64, C.c_int, C.c_int, _P, _P, _i64, _P, C.c_int,
+                             C.c_int, _P, _P], C.c_int),
 }
 
 EXPORTS = tuple(_SIGNATURES)

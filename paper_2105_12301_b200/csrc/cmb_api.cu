@@ -694,11 +694,77 @@ int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* est
   return CMB_OK;
 }
 
-int cmb_ccm_convergence(int, const double*, int64_t, int64_t, int, const int32_t*, const int32_t*,
-                        const int32_t*, int64_t, const int32_t*, int, int, const int32_t*,
-                        const int64_t*, double*) {
-  set_error("cmb_ccm_convergence is not implemented yet");
-  return CMB_ERR_UNSUPPORTED;
+int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E, int tau,
+                        const int32_t* lib_ids, const int32_t* tgt_ids, int64_t P,
+                        const int32_t* sizes, int n_sizes, int samples, const int32_t* pts,
+                        double* rho_out) {
+  CMB_TRY(check_spec(E, tau));
+  CMB_TRY(check_valid_count(len, E, tau));
+  CMB_PARAM(N >= 1 && P >= 0 && n_sizes >= 0 && samples >= 1, "bad sweep shape");
+  const int64_t n = len - (int64_t)(E - 1) * tau;
+  const int k = E + 1;
+  CMB_PARAM(k <= 31, "embedding dimension %d too large for the convergence sweep", E);
+  int64_t total_pts = 0;
+  std::vector<int64_t> size_off(n_sizes + 1, 0);
+  for (int s = 0; s < n_sizes; ++s) {
+    CMB_PARAM(sizes[s] >= E + 2 && sizes[s] <= n,
+              "library size %d outside [%d, %lld] (k = E + 1 neighbours excluding the point itself)",
+              sizes[s], E + 2, (long long)n);
+    size_off[s] = total_pts;
+    total_pts += (int64_t)sizes[s] * samples;
+  }
+  size_off[n_sizes] = total_pts;
+  for (int64_t q = 0; q < total_pts; ++q)
+    CMB_PARAM(pts[q] >= 0 && pts[q] < n, "library point %d outside [0, %lld)", pts[q], (long long)n);
+  for (int64_t p = 0; p < P; ++p)
+    CMB_PARAM(lib_ids[p] >= 0 && lib_ids[p] < N && tgt_ids[p] >= 0 && tgt_ids[p] < N, "bad pair %lld",
+              (long long)p);
+  if (P == 0 || n_sizes == 0) return CMB_OK;
+  CMB_CTX(dev);
+  CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * len));
+  CMB_CUDA(ctx->buf[B_A].ensure(sizeof(int32_t) * total_pts + 16));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X64].p, X, sizeof(double) * N * len, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_A].p, pts, sizeof(int32_t) * total_pts, cudaMemcpyHostToDevice, st));
+  const double* x64 = ctx->buf[B_X64].as<double>();
+  // pairs grouped by library
+  std::vector<std::vector<std::pair<int64_t, int>>> by_lib(N);
+  for (int64_t p = 0; p < P; ++p) by_lib[lib_ids[p]].push_back({p, tgt_ids[p]});
+  std::vector<double> host_rho;
+  for (int64_t lib = 0; lib < N; ++lib) {
+    const auto& pr = by_lib[lib];
+    if (pr.empty()) continue;
+    const int64_t M = (int64_t)pr.size();
+    CMB_CUDA(ctx->buf[B_C].ensure(sizeof(double) * M * len));
+    CMB_CUDA(ctx->buf[B_D].ensure(sizeof(double) * M * n));
+    CMB_CUDA(ctx->buf[B_E].ensure(sizeof(double) * M * n_sizes * samples));
+    for (int64_t m = 0; m < M; ++m)
+      CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_C].as<double>() + m * len, x64 + (int64_t)pr[m].second * len,
+                               sizeof(double) * len, cudaMemcpyDeviceToDevice, st));
+    for (int s = 0; s < n_sizes; ++s) {
+      CMB_CUDA(ctx->buf[B_B].ensure(sizeof(int64_t) * samples * n * k));
+      CMB_CUDA(ctx->buf[B_LIBCOL].ensure(sizeof(double) * samples * n * k));
+      CMB_CUDA(launch_restricted_tables(x64 + lib * len, (int)n, E, tau, k,
+                                        ctx->buf[B_A].as<int32_t>() + size_off[s], sizes[s], samples,
+                                        ctx->buf[B_B].as<int64_t>(), ctx->buf[B_LIBCOL].as<double>(), st));
+      for (int q = 0; q < samples; ++q) {
+        const size_t toff = (size_t)q * n * k;
+        CMB_CUDA(launch_lookup64(ctx->buf[B_B].as<int64_t>() + toff, ctx->buf[B_LIBCOL].as<double>() + toff,
+                                 n, k, (E - 1) * tau, ctx->buf[B_C].as<double>(), len, M,
+                                 ctx->buf[B_D].as<double>(),
+                                 ctx->buf[B_E].as<double>() + ((size_t)s * samples + q) * M, st));
+      }
+    }
+    host_rho.resize((size_t)M * n_sizes * samples);
+    CMB_CUDA(cudaMemcpyAsync(host_rho.data(), ctx->buf[B_E].p, sizeof(double) * host_rho.size(),
+                             cudaMemcpyDeviceToHost, st));
+    CMB_CUDA(cudaStreamSynchronize(st));
+    for (int64_t m = 0; m < M; ++m)
+      for (int s = 0; s < n_sizes; ++s)
+        for (int q = 0; q < samples; ++q)
+          rho_out[((size_t)pr[m].first * n_sizes + s) * samples + q] =
+              host_rho[((size_t)s * samples + q) * M + m];
+  }
+  return CMB_OK;
 }
 
 }  // extern "C"

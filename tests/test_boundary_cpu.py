@@ -100,3 +100,13 @@ def test_synthetic_generators_bit_identical_to_reference(golden):
     assert np.array_equal(P.mixed_dataset(20, 60, seed=1234, dtype=np.float64), g["syn_mixed60"])
     tiled = P.mixed_dataset(45, 60, seed=1234, dtype=np.float64)
     assert np.array_equal(tiled[:20], g["syn_mixed60"]) and tiled.shape == (45, 60)
+
+
+def test_convergence_sampling_matches_oracle_rule():
+    import crossmap_oracle as O
+    from paper_2105_12301_b200.convergence import sample_libraries
+    a = sample_libraries(500, [10, 100, 500], 4, seed=21)
+    b = O.sample_libraries(500, [10, 100, 500], 4, seed=21)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    with pytest.raises(P.ParameterError):
+        sample_libraries(50, [60], 1, seed=0)

@@ -264,3 +264,28 @@ def test_errors_surface_reference_types():
         P.lookup_batch(t, [np.zeros(40)])
     with pytest.raises(P.SeriesTooShortError):
         P.build_knn_table(np.arange(5, dtype=float), P.EmbeddingSpec(3, 1))
+
+
+# ---------------------------------------------------------------- convergence sweep (8f row 1)
+def test_ccm_convergence_matches_oracle_restatement():
+    pair = P.coupled_logistic(300, seed=3, beta=0.4)
+    x, y = pair[0].values, pair[1].values
+    sizes = [10, 40, 120, 297]
+    res = P.ccm(x, y, 2, sizes, samples=5, seed=11)
+    means, per = O.ccm_convergence(x, y, 2, 1, sizes, 5, seed=11)
+    assert np.allclose(res.rho, per, atol=1e-10, equal_nan=True)
+    assert np.allclose(res.mean, means, atol=1e-10, equal_nan=True)
+    # full library: every sample is the plain cross map (table on every point)
+    full = P.xmap(np.stack([x, y], axis=1), [2, 2])
+    assert abs(res.rho[-1, 0] - full[0, 1]) <= 1e-4
+
+
+def test_ccm_sweep_pairs_and_dimensions():
+    X = P.mixed_dataset(5, 250, seed=4).astype(np.float64)
+    E = np.array([1, 2, 3, 2, 1])
+    rho = P.convergence.ccm_sweep(X.T, E, [20, 60], samples=3, seed=2)
+    assert rho.shape == (25, 2, 3)
+    for p in (0, 7, 13, 24):
+        lib, tgt = divmod(p, 5)
+        _, per = O.ccm_convergence(X[lib], X[tgt], int(E[tgt]), 1, [20, 60], 3, seed=2)
+        assert np.allclose(rho[p], per, atol=1e-10, equal_nan=True), p
