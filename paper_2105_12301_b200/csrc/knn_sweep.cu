@@ -1,6 +1,8 @@
 // K1/K2 dispatch (kernel template in knn_sweep.cuh, instantiated per width in
 // knn_w*.cu) and the EDIM finalize kernel.
-#include "knn_sweep.cuh"
+#include "knn_tile.cuh"
+
+#include <cstdlib>
 
 namespace cmb {
 
@@ -10,6 +12,11 @@ CMB_W(1) CMB_W(2) CMB_W(3) CMB_W(4) CMB_W(5) CMB_W(6) CMB_W(7) CMB_W(8) CMB_W(9)
 CMB_W(11) CMB_W(12) CMB_W(13) CMB_W(14) CMB_W(15) CMB_W(16) CMB_W(17) CMB_W(18) CMB_W(19)
 CMB_W(20) CMB_W(24) CMB_W(28) CMB_W(30)
 #undef CMB_W
+#define CMB_T(n) extern template cudaError_t launch_tile_w<n>(const KnnArgs&, int, cudaStream_t);
+CMB_T(1) CMB_T(2) CMB_T(3) CMB_T(4) CMB_T(5) CMB_T(6) CMB_T(7) CMB_T(8) CMB_T(9) CMB_T(10)
+CMB_T(11) CMB_T(12) CMB_T(13) CMB_T(14) CMB_T(15) CMB_T(16) CMB_T(17) CMB_T(18) CMB_T(19)
+CMB_T(20)
+#undef CMB_T
 }  // namespace knn_detail
 
 using namespace knn_detail;
@@ -32,6 +39,21 @@ cudaError_t launch_knn_sweep(const KnnArgs& a_in, cudaStream_t st) {
   // float64 samples feed the exact re-rank (rare in TABLE mode: read them from L1/L2
   // there and keep shared memory for a third CTA per SM) and every EDIM/RAW row
   a.x64_smem = (a.mode != KNN_TABLE && (a.L + a.Tp) <= 6144) ? 1 : 0;
+  // tile kernel (knn_tile.cuh) for unit lag and widths <= 20 when selected with
+  // CMB_KNN_TILE=1 (A/B runs; it does not yet beat the v4 sweep)
+  static const bool use_tile = getenv("CMB_KNN_TILE") && getenv("CMB_KNN_TILE")[0] == '1';
+  const bool tile_ok = use_tile && a.tau == 1 && W <= 20 && (a.mode != KNN_RAW || a.k_raw <= 30) &&
+                       (a.L + a.Tp) <= 6144;
+  if (tile_ok) {
+    switch (W) {
+#define CMB_T(n) case n: return launch_tile_w<n>(a, grid, st);
+      CMB_T(1) CMB_T(2) CMB_T(3) CMB_T(4) CMB_T(5) CMB_T(6) CMB_T(7) CMB_T(8) CMB_T(9) CMB_T(10)
+      CMB_T(11) CMB_T(12) CMB_T(13) CMB_T(14) CMB_T(15) CMB_T(16) CMB_T(17) CMB_T(18) CMB_T(19)
+      CMB_T(20)
+#undef CMB_T
+      default: break;
+    }
+  }
   switch (W) {
 #define CMB_W(n) case n: return launch_w<n>(a, grid, st);
     CMB_W(1) CMB_W(2) CMB_W(3) CMB_W(4) CMB_W(5) CMB_W(6) CMB_W(7) CMB_W(8) CMB_W(9) CMB_W(10)

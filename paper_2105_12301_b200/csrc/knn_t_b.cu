@@ -1,0 +1,12 @@
+// Width instantiations of the K1/K2 tile kernel (split for parallel compilation).
+#include "knn_tile.cuh"
+
+namespace cmb {
+namespace knn_detail {
+template cudaError_t launch_tile_w<9>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_tile_w<10>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_tile_w<11>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_tile_w<12>(const KnnArgs&, int, cudaStream_t);
+template cudaError_t launch_tile_w<13>(const KnnArgs&, int, cudaStream_t);
+}  // namespace knn_detail
+}  // namespace cmb

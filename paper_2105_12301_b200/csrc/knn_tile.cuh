@@ -1,0 +1,534 @@
+// K1/K2 v6: two-pass register-window tile sweep (tau = 1).
+//
+// Same contract as knn_sweep_kernel (knn_sweep.cuh) -- every dimension
+// E <= E_HI of one library in one pass over the candidates, exact top-(E+1)
+// selection, TABLE / EDIM / RAW epilogues -- with a different selection
+// strategy, chosen from ncu captures (profiles/r01_*): in v4 the warp-uniform
+// threshold seeded from row i-1 was loose for noise-like series, 78% of the
+// (step, E) iterations took the ballot/insert path and the sweep ran at
+// ~2,500 warp instructions per (row, E); a first fully unrolled tile variant
+// cut the work but its 200 KB body stalled on instruction fetch (no_inst 85%),
+// so the hot loop here is a ~250-instruction block.
+//
+// Layout.  A warp owns one query row i at a time.  A tile is 768 candidates;
+// lane l owns two runs of 12 consecutive candidates half a tile apart,
+// p = tile0 + 12 l + c and p + 384 + c (c < 12).  The candidate window slides
+// by one sample per dimension (x[j + e], e = 0..E-1), so a block of four
+// dimensions needs only the 15 sample pairs (x[p+m], x[p+384+m]) -- loaded
+// once per block into registers from a pair-packed shared copy of the series
+// (one pad pair per 4, so the 32 lanes' 8-byte loads are bank-conflict free
+// and the offsets are compile-time constants) -- and each dimension is then
+// 12 FADD2 + 12 FFMA2 (sm_100 packed fp32) on registers.  Samples past the end
+// of the library are +inf, so a candidate's distance becomes +inf exactly at
+// the first dimension E with j >= n_E (no tail masking).
+//
+// Selection, per row:
+//   pass 1  distances of all tiles, per lane and dimension the running minimum
+//           over its candidates; the threshold t_E = the Kp-th smallest of the
+//           32 lane minima (Kp = k + 1 list entries) is an upper bound on the
+//           Kp-th smallest distance (Kp distinct lanes each hold a candidate
+//           <= t_E), tightened by the bound seeded from row i-1.
+//   pass 2  distances again; per (tile, E) a lane-min test against t_E, and
+//           when some lane has a candidate <= t_E the hitting lanes park their
+//           distances in a scratch row and an out-of-line collector appends
+//           the hits to the dimension's buffer.
+//   end     each buffer is sorted by (distance, index) (warp bitonic) into the
+//           list; certification, weights and records are the v4 epilogue.
+// Distances use exactly the v4 fp32 operation sequence (sub, then fma
+// accumulation in e order; the packed ops round identically), so the
+// certification bounds of knn_sweep.cuh apply unchanged.
+#pragma once
+
+#include "knn_sweep.cuh"
+
+namespace cmb {
+namespace knn_detail {
+
+constexpr int kRun = 12;              // consecutive candidates per run (two runs per lane)
+constexpr int kTC = 2 * kRun;         // candidates per lane per tile
+constexpr int kHalf = 32 * kRun;      // offset of the second run
+constexpr int kTile = 2 * kHalf;      // candidates per warp tile
+constexpr int kEB = 4;                // dimensions per unrolled block
+constexpr int kNW = kRun + kEB - 1;   // window pairs per block
+constexpr int kScr = kTC + 2;         // scratch row stride (floats): 8-byte aligned, conflict free
+constexpr int kScrWarp = 32 * kScr;   // per-warp scratch (also holds E_HI x 32 lane minima)
+
+// pair-packed series: pair p = (x[p], x[p + kHalf]) at index zi(p), one pad pair per 4
+__device__ __forceinline__ int zi(int p) { return p + (p >> 2); }
+__host__ __device__ constexpr int z_len(int n) { return n + (n >> 2) + 1; }
+__device__ __forceinline__ float xval(const float2* Z, int p) { return Z[zi(p)].x; }
+
+// candidate of hit bit c (c < kRun: first run, else second run) and its scratch slot
+__device__ __forceinline__ int cand_of(int p, int c) { return c < kRun ? p + c : p + kHalf + (c - kRun); }
+__device__ __forceinline__ int slot_of(int c) { return c < kRun ? 2 * c : 2 * (c - kRun) + 1; }
+
+// ascending bitonic sort of one float per lane
+__device__ __forceinline__ float warp_sort32f(float v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const float o = __shfl_xor_sync(CMB_FULL, v, stride);
+      const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+      v = keep_min ? fminf(v, o) : fmaxf(v, o);
+    }
+  }
+  return v;
+}
+
+// ascending bitonic sort of one key per lane over groups of W lanes
+template <int W>
+__device__ __forceinline__ unsigned long long warp_sortw(unsigned long long v) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= W; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      const unsigned long long o = __shfl_xor_sync(CMB_FULL, v, stride);
+      const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
+      v = keep_min ? (o < v ? o : v) : (o > v ? o : v);
+    }
+  }
+  return v;
+}
+
+// Merge buffer B[0, bc) (bc <= 32) into the sorted list L[0, lc); keep the Kp
+// smallest.  Sort width adapts to the buffer size.
+static __device__ __noinline__ int merge_buffer(Entry* L, const Entry* B, int lc, int bc, int Kp) {
+  const int lane = lane_id();
+  unsigned long long kb = kMaxKey, kl = kMaxKey;
+  if (lane < bc) kb = pack_key(B[lane].d, B[lane].j);
+  if (bc <= 8) kb = warp_sortw<8>(kb);
+  else if (bc <= 16) kb = warp_sortw<16>(kb);
+  else kb = warp_sortw<32>(kb);
+  if (lc == 0) {
+    __syncwarp();
+    if (lane < bc && lane < Kp) L[lane] = unpack_key(kb);
+    __syncwarp();
+    return min(Kp, bc);
+  }
+  if (lane < lc) kl = pack_key(L[lane].d, L[lane].j);
+  const int rb = lane + count_below(kl, kb);
+  const int rl = lane + count_below(kb, kl);
+  __syncwarp();
+  if (lane < bc && rb < Kp) L[rb] = unpack_key(kb);
+  if (lane < lc && rl < Kp) L[rl] = unpack_key(kl);
+  __syncwarp();
+  return min(Kp, lc + bc);
+}
+
+// Collect the lane's candidates at or below the dimension's threshold into
+// its hit buffer.  Every lane with a hit parked its 24 tile distances in its
+// scratch row (pair c at slots 2c, 2c + 1).  Common case: the hits fit the
+// buffer and are appended at warp-prefix offsets; otherwise (many candidates
+// at the threshold, e.g. ties in integer-valued or constant stretches) they
+// are appended in ballot rounds, merging the buffer into the list whenever it
+// would overflow, which tightens the threshold.
+static __device__ __noinline__ void collect_hits(const float* scr, bool has, Entry* Le, Entry* Be,
+                                                 int* cnt, float* thr_slot, int p, int Kp,
+                                                 unsigned long long* diag) {
+  const int lane = lane_id();
+  float t = *thr_slot;
+  unsigned hm = 0;
+  if (has) {
+#pragma unroll
+    for (int c = 0; c < kRun; ++c) {
+      const float2 v = *reinterpret_cast<const float2*>(scr + 2 * c);
+      hm |= (v.x <= t ? 1u : 0u) << c;
+      hm |= (v.y <= t ? 1u : 0u) << (c + kRun);
+    }
+  }
+  const int n = __popc(hm);
+  int incl = n;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(CMB_FULL, incl, o);
+    if (lane >= o) incl += u;
+  }
+  const int total = __shfl_sync(CMB_FULL, incl, 31);
+  int bc = cnt[1];
+#ifdef CMB_KNN_STATS
+  if (diag && lane == 0) {
+    atomicAdd(diag + 3, (unsigned long long)total);
+    atomicAdd(diag + 4, 1ull);
+    if (bc + total > kCap) atomicAdd(diag + 5, 1ull);
+  }
+#endif
+  if (bc + total <= kCap) {
+    Entry* dst = Be + bc + incl - n;
+    while (hm) {
+      const int c = __ffs(hm) - 1;
+      hm &= hm - 1;
+      Entry h;
+      h.d = scr[slot_of(c)];
+      h.j = cand_of(p, c);
+      *dst++ = h;
+    }
+    bc += total;
+  } else {
+    const unsigned below = (1u << lane) - 1u;
+#pragma unroll 1
+    for (int c = 0; c < kTC; ++c) {
+      const float vc = has ? scr[slot_of(c)] : kInfF;
+      unsigned m = __ballot_sync(CMB_FULL, vc <= t);
+      if (!m) continue;
+      if (bc + __popc(m) > kCap) {
+        __syncwarp();
+        const int lc = merge_buffer(Le, Be, cnt[0], bc, Kp);
+        if (lane == 0) cnt[0] = lc;
+        bc = 0;
+        if (lc == Kp) t = fminf(t, Le[Kp - 1].d);
+        __syncwarp();
+        m = __ballot_sync(CMB_FULL, vc <= t);
+      }
+      if ((m >> lane) & 1u) {
+        Entry h;
+        h.d = vc;
+        h.j = cand_of(p, c);
+        Be[bc + __popc(m & below)] = h;
+      }
+      bc += __popc(m);
+    }
+  }
+  __syncwarp();
+  if (lane == 0) {
+    cnt[1] = bc;
+    *thr_slot = t;
+  }
+  __syncwarp();
+}
+
+// Thresholds after pass 1: per active dimension the Kp-th smallest of the 32
+// lane minima (mins[e][lane]), tightened by the seeded bound in thr[e].
+static __device__ __noinline__ void lane_min_thresholds(const float* mins, float* thr, uint32_t act,
+                                                        int mode, int k_raw, int L) {
+  const int lane = lane_id();
+  uint32_t m = act;
+  while (m) {
+    const int e = __ffs(m) - 1;
+    m &= m - 1;
+    const float s = warp_sort32f(mins[e * 32 + lane]);
+    const float t = fminf(thr[e], __shfl_sync(CMB_FULL, s, kp_of(mode, k_raw, L, 1, e) - 1));
+    __syncwarp();
+    if (lane == 0) thr[e] = t;
+    __syncwarp();
+  }
+}
+
+// Threshold seed for row i from row i-1's final list shifted by one sample
+// (padded series layout).  Returns +inf when no valid seed exists.
+static __device__ __noinline__ float seed_tile(const Entry* Le, const float2* __restrict__ Z, int i,
+                                               int e, int nE, int Kp) {
+  const int lane = lane_id();
+  bool ok = true;
+  float ds = -kInfF;
+  if (lane < Kp) {
+    const int jp = Le[lane].j;
+    const int js = jp + 1;
+    ok = jp != kNoJ && js < nE && js != i;
+    if (ok) {
+      float dv = 0.f;
+      for (int q = 0; q <= e; ++q) {
+        const float df = __fsub_rn(xval(Z, js + q), xval(Z, i + q));
+        dv = __fmaf_rn(df, df, dv);
+      }
+      ds = dv;
+    }
+  }
+  float thr = kInfF;
+  if (__all_sync(CMB_FULL, ok)) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ds = fmaxf(ds, __shfl_xor_sync(CMB_FULL, ds, o));
+    if (ds < kInfF) thr = __int_as_float(__float_as_int(ds) + 1);  // next float above
+  }
+  return thr;
+}
+
+// Window of one dimension block and the initial distances of the lane's 24
+// candidates (pair c = candidates p + c and p + kHalf + c).
+__device__ __forceinline__ void block_window(const float2* __restrict__ Z, int zb, int eb,
+                                             float2 (&W)[kNW]) {
+  const float2* zp = Z + zb + (kEB + 1) * eb;  // zi(p + kEB eb + m) = zb + 5 eb + m + m / 4
+#pragma unroll
+  for (int m = 0; m < kNW; ++m) W[m] = zp[m + (m >> 2)];
+}
+
+__device__ __forceinline__ float tile_min(const float2 (&D)[kRun]) {
+  float m[kRun / 3];
+#pragma unroll
+  for (int q = 0; q < kRun / 3; ++q)
+    m[q] = fminf(fminf(fminf(D[3 * q].x, D[3 * q].y), fminf(D[3 * q + 1].x, D[3 * q + 1].y)),
+                 fminf(D[3 * q + 2].x, D[3 * q + 2].y));
+  return fminf(fminf(m[0], m[1]), fminf(m[2], m[3]));
+}
+
+template <int E_HI>
+__global__ void __launch_bounds__(kThreads, 2)
+knn_tile_kernel(const __grid_constant__ KnnArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  constexpr int LT = list_total<E_HI>();
+  constexpr int EHR = (E_HI + kEB - 1) / kEB * kEB;  // dimensions rounded up to whole blocks
+  __shared__ double red[kWarps][E_HI][5];
+  __shared__ float thr_s[kWarps][E_HI];
+  __shared__ float2 nq_s[kWarps][EHR];
+  __shared__ int cnt_s[kWarps][E_HI][2];
+  __shared__ double s_mean;
+  __shared__ int s_last;
+
+  const int lib = blockIdx.x / a.nrb;
+  const int rb = blockIdx.x - lib * a.nrb;
+  const int64_t srow = a.lib_rows ? a.lib_rows[lib] : lib;
+  const float* __restrict__ gx = a.x32 + srow * a.ld;
+  const double* __restrict__ gx64 = a.x64 + srow * a.ld;
+  const int L = a.L;
+  const int Tfull = L + a.Tp;
+  const int lane = lane_id(), w = warp_id();
+
+  Entry* lists = reinterpret_cast<Entry*>(smem);
+  Entry* bufs = lists + kWarps * LT;
+  float* scratch = reinterpret_cast<float*>(bufs + kWarps * E_HI * kCap);
+  double* x64s = reinterpret_cast<double*>(scratch + kWarps * kScrWarp);
+  const int x64n = a.x64_smem ? ((Tfull + 1) & ~1) : 0;
+  float2* Z = reinterpret_cast<float2*>(x64s + x64n);
+
+  // stage the library series as (x[p], x[p + kHalf]) pairs, +inf past the end
+  const int zspan = L + kHalf + 32 + EHR;
+  for (int q = threadIdx.x; q < zspan; q += kThreads) {
+    float2 v;
+    v.x = (q < L) ? gx[q] : kInfF;
+    v.y = (q + kHalf < L) ? gx[q + kHalf] : kInfF;
+    Z[zi(q)] = v;
+  }
+  if (a.x64_smem)
+    for (int t = threadIdx.x; t < Tfull; t += kThreads) x64s[t] = gx64[t];
+  const double* __restrict__ xp = a.x64_smem ? x64s : gx64;
+
+  if (a.mode == KNN_EDIM) {
+    double s = 0.0;
+    int last = 0;
+    for (int t = threadIdx.x; t < Tfull; t += kThreads) {
+      const double v = gx64[t];
+      s += v;
+      if (t > 0 && v != gx64[t - 1]) last = max(last, t);
+    }
+    s = warp_sum_d(s);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) last = max(last, __shfl_xor_sync(CMB_FULL, last, o));
+    __shared__ double ws[kWarps];
+    __shared__ int wl[kWarps];
+    if (lane == 0) { ws[w] = s; wl[w] = last; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0.0;
+      int lst = 0;
+      for (int q = 0; q < kWarps; ++q) { tot += ws[q]; lst = max(lst, wl[q]); }
+      s_mean = tot / Tfull;
+      s_last = lst;
+    }
+  }
+  __syncthreads();
+
+  const double M = a.err_m ? (double)a.err_m[lib] : 0.0;
+  const int e_hi = a.e_hi;
+  const int rpw = (a.rows_per_block + kWarps - 1) / kWarps;
+  const int r0 = rb * a.rows_per_block + w * rpw;
+  const int r1 = min(min(L, rb * a.rows_per_block + a.rows_per_block), r0 + rpw);
+  Entry* wl = lists + w * LT;
+  Entry* wb = bufs + w * E_HI * kCap;
+  float* wscr = scratch + w * kScrWarp;
+  float* mins = wscr;  // pass 1 / thresholds: [e][lane] (the scratch is free until pass 2)
+  int* wc = &cnt_s[w][0][0];
+
+  double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, acc4 = 0;
+  const double shift = (a.mode == KNN_EDIM) ? s_mean : 0.0;
+  uint32_t prev_act = 0;
+
+  for (int i = max(0, r0 - 1); i < r1; ++i) {
+    const bool emit = i >= r0;
+    uint32_t act = 0;
+    for (int e = 0; e < e_hi; ++e)
+      if (((a.need >> e) & 1u) && i < L - e) act |= 1u << e;
+    if (!act) { prev_act = 0; continue; }
+    const int eh = 32 - __clz(act);
+    const int nb = (eh + kEB - 1) / kEB;
+
+    // ---- seeds from row i-1, list/buffer reset, query coordinates, pass-1 minima
+#pragma unroll 1
+    for (int e = 0; e < eh; ++e) {
+      if (!((act >> e) & 1u)) continue;
+      const int Kp = kp_of(a.mode, a.k_raw, L, 1, e);
+      float thr = kInfF;
+      if ((prev_act >> e) & 1u) thr = seed_tile(list_of(wl, a.mode, e), Z, i, e, L - e, Kp);
+      __syncwarp();
+      if (lane == 0) {
+        wc[2 * e] = 0;
+        wc[2 * e + 1] = 0;
+        thr_s[w][e] = thr;
+      }
+    }
+    if (lane < EHR) {
+      const float q = (lane < eh) ? xval(Z, i + lane) : 0.f;
+      nq_s[w][lane] = make_float2(-q, -q);
+    }
+    for (int e = 0; e < eh; ++e) mins[e * 32 + lane] = kInfF;
+    __syncwarp();
+
+    // ---- pass 1: per-lane minima
+    for (int tile0 = 0; tile0 < L; tile0 += kTile) {
+      const int p = tile0 + kRun * lane;
+      const int zb = zi(p);
+      float2 D[kRun];
+#pragma unroll
+      for (int c = 0; c < kRun; ++c) {
+        D[c].x = (p + c == i) ? kInfF : 0.f;
+        D[c].y = (p + kHalf + c == i) ? kInfF : 0.f;
+      }
+#pragma unroll 1
+      for (int eb = 0; eb < nb; ++eb) {
+        float2 W[kNW];
+        block_window(Z, zb, eb, W);
+#pragma unroll
+        for (int r = 0; r < kEB; ++r) {
+          const int e = kEB * eb + r;
+          if (e < eh) {
+            const float2 nq = nq_s[w][e];
+#pragma unroll
+            for (int c = 0; c < kRun; ++c) {
+              const float2 df = __fadd2_rn(W[c + r], nq);
+              D[c] = __ffma2_rn(df, df, D[c]);
+            }
+            if ((act >> e) & 1u) mins[e * 32 + lane] = fminf(mins[e * 32 + lane], tile_min(D));
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // thresholds: Kp-th smallest lane minimum, tightened by the seed
+    lane_min_thresholds(mins, thr_s[w], act, a.mode, a.k_raw, L);
+
+    // ---- pass 2: collect candidates at or below the thresholds
+    for (int tile0 = 0; tile0 < L; tile0 += kTile) {
+      const int p = tile0 + kRun * lane;
+      const int zb = zi(p);
+      float2 D[kRun];
+#pragma unroll
+      for (int c = 0; c < kRun; ++c) {
+        D[c].x = (p + c == i) ? kInfF : 0.f;
+        D[c].y = (p + kHalf + c == i) ? kInfF : 0.f;
+      }
+#pragma unroll 1
+      for (int eb = 0; eb < nb; ++eb) {
+        float2 W[kNW];
+        block_window(Z, zb, eb, W);
+#pragma unroll
+        for (int r = 0; r < kEB; ++r) {
+          const int e = kEB * eb + r;
+          if (e < eh) {
+            const float2 nq = nq_s[w][e];
+#pragma unroll
+            for (int c = 0; c < kRun; ++c) {
+              const float2 df = __fadd2_rn(W[c + r], nq);
+              D[c] = __ffma2_rn(df, df, D[c]);
+            }
+            if ((act >> e) & 1u) {
+              const float t = thr_s[w][e];
+              const bool has = tile_min(D) <= t;
+              if (__any_sync(CMB_FULL, has)) {
+                if (has) {
+#pragma unroll
+                  for (int c = 0; c < kRun; ++c) *reinterpret_cast<float2*>(wscr + lane * kScr + 2 * c) = D[c];
+                }
+                __syncwarp();
+                collect_hits(wscr + lane * kScr, has, list_of(wl, a.mode, e), wb + e * kCap, wc + 2 * e,
+                             &thr_s[w][e], p, kp_of(a.mode, a.k_raw, L, 1, e), a.diag);
+              }
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- end of row: sort the buffers into the lists
+#pragma unroll 1
+    for (int e = 0; e < eh; ++e) {
+      if (!((act >> e) & 1u)) continue;
+      int* cnt = wc + 2 * e;
+      const int bc = cnt[1];
+      if (bc > 0) {
+        const int lc = merge_buffer(list_of(wl, a.mode, e), wb + e * kCap, cnt[0], bc, kp_of(a.mode, a.k_raw, L, 1, e));
+        __syncwarp();
+        if (lane == 0) {
+          cnt[0] = lc;
+          cnt[1] = 0;
+        }
+      }
+    }
+    __syncwarp();
+
+    // ---- certification, weights, records / predictions (v4 epilogue)
+    unsigned need = lane_finish<E_HI>(&a, wl, wb, wc, lib, i, act, M, emit);
+    __syncwarp();
+#pragma unroll 1
+    while (need) {
+      const int e = __ffs(need) - 1;
+      need &= need - 1;
+      const PredObs po = epilogue_e<E_HI>(&a, list_of(wl, a.mode, e), lib, i, e, xp, M, shift);
+      if (a.mode == KNN_EDIM && lane == e) {
+        acc0 += po.o;
+        acc1 += po.p;
+        acc2 += po.o * po.o;
+        acc3 += po.p * po.p;
+        acc4 += po.o * po.p;
+      }
+    }
+    prev_act = act;
+    __syncwarp();
+  }
+
+  if (a.mode == KNN_EDIM) {
+    if (lane < E_HI) {
+      red[w][lane][0] = acc0;
+      red[w][lane][1] = acc1;
+      red[w][lane][2] = acc2;
+      red[w][lane][3] = acc3;
+      red[w][lane][4] = acc4;
+    }
+    __syncthreads();
+    if (threadIdx.x < e_hi * 5) {
+      const int e = threadIdx.x / 5, c = threadIdx.x % 5;
+      double s = 0.0;
+      for (int q = 0; q < kWarps; ++q) s += red[q][e][c];
+      a.part[(((size_t)lib * a.nrb + rb) * e_hi + e) * 5 + c] = s;
+    }
+    if (rb == 0 && threadIdx.x == 0) {
+      a.last_change[lib] = s_last;
+      a.mean[lib] = s_mean;
+    }
+  }
+}
+
+template <int W>
+size_t tile_smem_bytes(const KnnArgs& a) {
+  const int Tfull = a.L + a.Tp;
+  size_t b = sizeof(Entry) * kWarps * (list_total<W>() + W * kCap);
+  b += sizeof(float) * (kWarps * kScrWarp);
+  if (a.x64_smem) b += sizeof(double) * ((Tfull + 1) & ~1);
+  b += sizeof(float2) * (size_t)z_len(a.L + kHalf + 32 + (W + kEB - 1) / kEB * kEB);
+  return b;
+}
+
+template <int W>
+cudaError_t launch_tile_w(const KnnArgs& a, int grid, cudaStream_t st) {
+  auto kern = knn_tile_kernel<W>;
+  const size_t smem = tile_smem_bytes<W>(a);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  count_launch();
+  kern<<<grid, kThreads, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace knn_detail
+}  // namespace cmb
