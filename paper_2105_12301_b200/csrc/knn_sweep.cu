@@ -39,12 +39,13 @@ cudaError_t launch_knn_sweep(const KnnArgs& a_in, cudaStream_t st) {
   // float64 samples feed the exact re-rank (rare in TABLE mode: read them from L1/L2
   // there and keep shared memory for a third CTA per SM) and every EDIM/RAW row
   a.x64_smem = (a.mode != KNN_TABLE && (a.L + a.Tp) <= 6144) ? 1 : 0;
-  // tile kernel (knn_tile.cuh) for unit lag and widths <= 20 when selected with
-  // CMB_KNN_TILE=1 (A/B runs; it does not yet beat the v4 sweep)
-  static const bool use_tile = getenv("CMB_KNN_TILE") && getenv("CMB_KNN_TILE")[0] == '1';
-  const bool tile_ok = use_tile && a.tau == 1 && W <= 20 && (a.mode != KNN_RAW || a.k_raw <= 30) &&
+  // tile kernel (knn_tile.cuh) for unit lag and widths <= 20; the v4 sweep covers
+  // tau > 1, wider sweeps, long RAW lists, and CMB_KNN_V4=1 (A/B runs)
+  static const bool force_v4 = getenv("CMB_KNN_V4") && getenv("CMB_KNN_V4")[0] == '1';
+  const bool tile_ok = !force_v4 && a.tau == 1 && W <= 20 && (a.mode != KNN_RAW || a.k_raw <= 30) &&
                        (a.L + a.Tp) <= 6144;
   if (tile_ok) {
+    a.x64_smem = 0;  // the tile kernel reads the float64 series (exact re-rank) through L1
     switch (W) {
 #define CMB_T(n) case n: return launch_tile_w<n>(a, grid, st);
       CMB_T(1) CMB_T(2) CMB_T(3) CMB_T(4) CMB_T(5) CMB_T(6) CMB_T(7) CMB_T(8) CMB_T(9) CMB_T(10)

@@ -209,6 +209,10 @@ static __device__ __noinline__ int compact_lists(Entry* L, Entry* B, int lc, int
   return min(Kp, lc + bc);
 }
 
+// Tile-kernel hit buffers (knn_tile.cuh): kCap entries per dimension; a RAW
+// sweep (one list) uses the first.
+__device__ __forceinline__ int tile_buf_off(int mode, int e) { return mode == KNN_RAW ? 0 : e * kCap; }
+
 struct RowCtx {
   int i, L, tau, mode, k_raw;
   uint32_t act;
@@ -378,14 +382,15 @@ struct PredObs {
 template <int E_HI>
 static __device__ __noinline__ unsigned lane_finish(const KnnArgs* __restrict__ ap, Entry* wl,
                                                     Entry* wb, int* wc, int lib, int i,
-                                                    uint32_t act, double M, bool emit) {
+                                                    uint32_t act, double M, bool emit,
+                                                    bool tile_layout = false) {
   const KnnArgs& a = *ap;
   const int lane = lane_id();
   const int e = lane;
   bool pending = false;
   if (e < E_HI && ((act >> e) & 1u)) {
     Entry* Le = list_of(wl, a.mode, e);
-    const Entry* Be = wb + e * kCap;
+    const Entry* Be = wb + (tile_layout ? tile_buf_off(a.mode, e) : e * kCap);
     int* c = wc + 2 * e;
     const int Kp = kp_of(a.mode, a.k_raw, a.L, a.tau, e);
     int lc = c[0];

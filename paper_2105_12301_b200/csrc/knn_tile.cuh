@@ -51,7 +51,7 @@ constexpr int kTile = 2 * kHalf;      // candidates per warp tile
 constexpr int kEB = 4;                // dimensions per unrolled block
 constexpr int kNW = kRun + kEB - 1;   // window pairs per block
 constexpr int kScr = kTC + 2;         // scratch row stride (floats): 8-byte aligned, conflict free
-constexpr int kScrWarp = 32 * kScr;   // per-warp scratch (also holds E_HI x 32 lane minima)
+constexpr int kScrWarp = 768;        // per-warp scratch: a tile's pool, or E_HI x 33 lane minima
 
 // pair-packed series: pair p = (x[p], x[p + kHalf]) at index zi(p), one pad pair per 4
 __device__ __forceinline__ int zi(int p) { return p + (p >> 2); }
@@ -118,131 +118,111 @@ static __device__ __noinline__ int merge_buffer(Entry* L, const Entry* B, int lc
   return min(Kp, lc + bc);
 }
 
-// Collect the lane's candidates at or below the dimension's threshold into
-// its hit buffer.  Every lane with a hit parked its 24 tile distances in its
-// scratch row (pair c at slots 2c, 2c + 1).  Common case: the hits fit the
-// buffer and are appended at warp-prefix offsets; otherwise (many candidates
-// at the threshold, e.g. ties in integer-valued or constant stretches) they
-// are appended in ballot rounds, merging the buffer into the list whenever it
-// would overflow, which tightens the threshold.
-static __device__ __noinline__ void collect_hits(const float* scr, bool has, Entry* Le, Entry* Be,
-                                                 int* cnt, float* thr_slot, int p, int Kp,
-                                                 unsigned long long* diag) {
+// Thresholds after pass 1, lane-parallel: lane e sorts the 32 lane minima of
+// dimension e (mins[e * kMinStride + q]) with a register bitonic network and
+// takes the Kp-th smallest.  It is an upper bound on the Kp-th smallest
+// distance (Kp distinct lanes each hold a candidate at or below it).  ntp[e] =
+// -(next float above t) in both halves: D <= t  <=>  D + ntp < 0 (exact: a
+// difference of distinct floats never rounds to zero without flush-to-zero).
+constexpr int kMinStride = 33;  // conflict-free transposed reads
+static __device__ __noinline__ void lane_min_thresholds(const float* mins, float* thr, float2* ntp,
+                                                        uint32_t act, int mode, int k_raw, int L) {
+  const int e = lane_id();
+  if (e < 32 && ((act >> e) & 1u)) {
+    float v[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) v[q] = mins[e * kMinStride + q];
+#pragma unroll
+    for (int size = 2; size <= 32; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int r = q ^ stride;
+          if (r > q) {
+            const float lo = fminf(v[q], v[r]), hi = fmaxf(v[q], v[r]);
+            const bool up = (q & size) == 0;
+            v[q] = up ? lo : hi;
+            v[r] = up ? hi : lo;
+          }
+        }
+      }
+    }
+    const int kp = kp_of(mode, k_raw, L, 1, e);
+    float t = v[0];
+#pragma unroll
+    for (int q = 1; q < 32; ++q) t = (q == kp - 1) ? v[q] : t;
+    const float tn = (t < kInfF) ? -__int_as_float(__float_as_int(t) + 1) : -kInfF;
+    thr[e] = t;
+    ntp[e] = make_float2(tn, tn);
+  }
+  __syncwarp();
+}
+
+// Pool round: each lane takes one pool candidate j (or none; the pool is in
+// increasing j), recomputes its distances for every dimension in the sweep's
+// exact fp32 operation order, and the warp appends the hits (D_e(j) <= t_e) to
+// the dimension buffers by ballot.  Buffer counts live in lane e's register
+// (bc); a buffer that would overflow is first merged into its list, which
+// tightens the threshold to strictly below the list's last distance.  Buffer
+// order is otherwise irrelevant (lane_finish inserts by (distance, index)).
+static __device__ __noinline__ int pool_round(const int* pool, int n, const float2* __restrict__ Z,
+                                              const float2* nq, float* thr, int* wc, Entry* wl, Entry* wb,
+                                              uint32_t act, int eh, int mode, int k_raw, int L, int bc,
+                                              unsigned long long* g_stats) {
   const int lane = lane_id();
-  float t = *thr_slot;
-  unsigned hm = 0;
-  if (has) {
-#pragma unroll
-    for (int c = 0; c < kRun; ++c) {
-      const float2 v = *reinterpret_cast<const float2*>(scr + 2 * c);
-      hm |= (v.x <= t ? 1u : 0u) << c;
-      hm |= (v.y <= t ? 1u : 0u) << (c + kRun);
-    }
-  }
-  const int n = __popc(hm);
-  int incl = n;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(CMB_FULL, incl, o);
-    if (lane >= o) incl += u;
-  }
-  const int total = __shfl_sync(CMB_FULL, incl, 31);
-  int bc = cnt[1];
-#ifdef CMB_KNN_STATS
-  if (diag && lane == 0) {
-    atomicAdd(diag + 3, (unsigned long long)total);
-    atomicAdd(diag + 4, 1ull);
-    if (bc + total > kCap) atomicAdd(diag + 5, 1ull);
-  }
-#endif
-  if (bc + total <= kCap) {
-    Entry* dst = Be + bc + incl - n;
-    while (hm) {
-      const int c = __ffs(hm) - 1;
-      hm &= hm - 1;
-      Entry h;
-      h.d = scr[slot_of(c)];
-      h.j = cand_of(p, c);
-      *dst++ = h;
-    }
-    bc += total;
-  } else {
-    const unsigned below = (1u << lane) - 1u;
+  const unsigned below = (1u << lane) - 1u;
+  const bool valid = lane < n;
+  const int j = valid ? pool[lane] : 0;
+  float d = valid ? 0.f : kInfF;
+  const float2* zj = Z + zi(j);
 #pragma unroll 1
-    for (int c = 0; c < kTC; ++c) {
-      const float vc = has ? scr[slot_of(c)] : kInfF;
-      unsigned m = __ballot_sync(CMB_FULL, vc <= t);
-      if (!m) continue;
-      if (bc + __popc(m) > kCap) {
-        __syncwarp();
-        const int lc = merge_buffer(Le, Be, cnt[0], bc, Kp);
-        if (lane == 0) cnt[0] = lc;
-        bc = 0;
-        if (lc == Kp) t = fminf(t, Le[Kp - 1].d);
-        __syncwarp();
-        m = __ballot_sync(CMB_FULL, vc <= t);
+  for (int e = 0; e < eh; ++e) {
+    const float xv = valid ? Z[zi(j + e)].x : 0.f;
+    const float df = __fadd_rn(xv, nq[e].x);
+    d = __fmaf_rn(df, df, d);
+    if (!((act >> e) & 1u)) continue;
+    unsigned m = __ballot_sync(CMB_FULL, d <= thr[e]);
+    if (!m) continue;
+    int b0 = __shfl_sync(CMB_FULL, bc, e);
+    Entry* Be = wb + tile_buf_off(mode, e);
+#ifdef CMB_KNN_STATS
+    if (lane == 0 && g_stats) atomicAdd(g_stats + 0, (unsigned long long)__popc(m));
+#endif
+    if (b0 + __popc(m) > kCap) {
+#ifdef CMB_KNN_STATS
+      if (lane == 0 && g_stats) atomicAdd(g_stats + 1, 1ull);
+#endif
+      const int Kp = kp_of(mode, k_raw, L, 1, e);
+      Entry* Le = list_of(wl, mode, e);
+      const int lc = merge_buffer(Le, Be, wc[2 * e], b0, Kp);
+      // pool candidates arrive in increasing j, so once the list is full a later
+      // candidate enters only with a strictly smaller distance than its last entry
+      float t2 = thr[e];
+      if (lc == Kp) {
+        const float last = Le[Kp - 1].d;
+        const float below = last > 0.f ? __int_as_float(__float_as_int(last) - 1) : -1.f;
+        t2 = fminf(t2, below);
       }
-      if ((m >> lane) & 1u) {
-        Entry h;
-        h.d = vc;
-        h.j = cand_of(p, c);
-        Be[bc + __popc(m & below)] = h;
+      __syncwarp();
+      if (lane == 0) {
+        wc[2 * e] = lc;
+        thr[e] = t2;
       }
-      bc += __popc(m);
+      b0 = 0;
+      m = __ballot_sync(CMB_FULL, d <= t2);
     }
-  }
-  __syncwarp();
-  if (lane == 0) {
-    cnt[1] = bc;
-    *thr_slot = t;
-  }
-  __syncwarp();
-}
-
-// Thresholds after pass 1: per active dimension the Kp-th smallest of the 32
-// lane minima (mins[e][lane]), tightened by the seeded bound in thr[e].
-static __device__ __noinline__ void lane_min_thresholds(const float* mins, float* thr, uint32_t act,
-                                                        int mode, int k_raw, int L) {
-  const int lane = lane_id();
-  uint32_t m = act;
-  while (m) {
-    const int e = __ffs(m) - 1;
-    m &= m - 1;
-    const float s = warp_sort32f(mins[e * 32 + lane]);
-    const float t = fminf(thr[e], __shfl_sync(CMB_FULL, s, kp_of(mode, k_raw, L, 1, e) - 1));
-    __syncwarp();
-    if (lane == 0) thr[e] = t;
-    __syncwarp();
-  }
-}
-
-// Threshold seed for row i from row i-1's final list shifted by one sample
-// (padded series layout).  Returns +inf when no valid seed exists.
-static __device__ __noinline__ float seed_tile(const Entry* Le, const float2* __restrict__ Z, int i,
-                                               int e, int nE, int Kp) {
-  const int lane = lane_id();
-  bool ok = true;
-  float ds = -kInfF;
-  if (lane < Kp) {
-    const int jp = Le[lane].j;
-    const int js = jp + 1;
-    ok = jp != kNoJ && js < nE && js != i;
-    if (ok) {
-      float dv = 0.f;
-      for (int q = 0; q <= e; ++q) {
-        const float df = __fsub_rn(xval(Z, js + q), xval(Z, i + q));
-        dv = __fmaf_rn(df, df, dv);
-      }
-      ds = dv;
+    if ((m >> lane) & 1u) {
+      Entry h;
+      h.d = d;
+      h.j = j;
+      Be[b0 + __popc(m & below)] = h;
     }
+    if (lane == e) bc = b0 + __popc(m);
   }
-  float thr = kInfF;
-  if (__all_sync(CMB_FULL, ok)) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ds = fmaxf(ds, __shfl_xor_sync(CMB_FULL, ds, o));
-    if (ds < kInfF) thr = __int_as_float(__float_as_int(ds) + 1);  // next float above
-  }
-  return thr;
+  (void)zj;
+  __syncwarp();
+  return bc;
 }
 
 // Window of one dimension block and the initial distances of the lane's 24
@@ -269,9 +249,9 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   constexpr int LT = list_total<E_HI>();
   constexpr int EHR = (E_HI + kEB - 1) / kEB * kEB;  // dimensions rounded up to whole blocks
-  __shared__ double red[kWarps][E_HI][5];
   __shared__ float thr_s[kWarps][E_HI];
   __shared__ float2 nq_s[kWarps][EHR];
+  __shared__ float2 ntp_s[kWarps][E_HI];
   __shared__ int cnt_s[kWarps][E_HI][2];
   __shared__ double s_mean;
   __shared__ int s_last;
@@ -288,6 +268,8 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
   Entry* lists = reinterpret_cast<Entry*>(smem);
   Entry* bufs = lists + kWarps * LT;
   float* scratch = reinterpret_cast<float*>(bufs + kWarps * E_HI * kCap);
+  // EDIM reduction after the row loop reuses the (then idle) hit buffers
+  double (*red)[E_HI][5] = reinterpret_cast<double (*)[E_HI][5]>(bufs);
   double* x64s = reinterpret_cast<double*>(scratch + kWarps * kScrWarp);
   const int x64n = a.x64_smem ? ((Tfull + 1) & ~1) : 0;
   float2* Z = reinterpret_cast<float2*>(x64s + x64n);
@@ -342,36 +324,27 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
 
   double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, acc4 = 0;
   const double shift = (a.mode == KNN_EDIM) ? s_mean : 0.0;
-  uint32_t prev_act = 0;
 
   for (int i = max(0, r0 - 1); i < r1; ++i) {
     const bool emit = i >= r0;
     uint32_t act = 0;
     for (int e = 0; e < e_hi; ++e)
       if (((a.need >> e) & 1u) && i < L - e) act |= 1u << e;
-    if (!act) { prev_act = 0; continue; }
+    if (!act) continue;
     const int eh = 32 - __clz(act);
     const int nb = (eh + kEB - 1) / kEB;
 
-    // ---- seeds from row i-1, list/buffer reset, query coordinates, pass-1 minima
-#pragma unroll 1
-    for (int e = 0; e < eh; ++e) {
-      if (!((act >> e) & 1u)) continue;
-      const int Kp = kp_of(a.mode, a.k_raw, L, 1, e);
-      float thr = kInfF;
-      if ((prev_act >> e) & 1u) thr = seed_tile(list_of(wl, a.mode, e), Z, i, e, L - e, Kp);
-      __syncwarp();
-      if (lane == 0) {
-        wc[2 * e] = 0;
-        wc[2 * e + 1] = 0;
-        thr_s[w][e] = thr;
-      }
+    // ---- list/buffer reset, query coordinates, pass-1 minima
+    if (lane < E_HI) {
+      wc[2 * lane] = 0;
+      wc[2 * lane + 1] = 0;
+      thr_s[w][lane] = kInfF;
     }
     if (lane < EHR) {
       const float q = (lane < eh) ? xval(Z, i + lane) : 0.f;
       nq_s[w][lane] = make_float2(-q, -q);
     }
-    for (int e = 0; e < eh; ++e) mins[e * 32 + lane] = kInfF;
+    for (int e = 0; e < eh; ++e) mins[e * kMinStride + lane] = kInfF;
     __syncwarp();
 
     // ---- pass 1: per-lane minima
@@ -398,24 +371,28 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
               const float2 df = __fadd2_rn(W[c + r], nq);
               D[c] = __ffma2_rn(df, df, D[c]);
             }
-            if ((act >> e) & 1u) mins[e * 32 + lane] = fminf(mins[e * 32 + lane], tile_min(D));
+            if ((act >> e) & 1u) mins[e * kMinStride + lane] = fminf(mins[e * kMinStride + lane], tile_min(D));
           }
         }
       }
     }
     __syncwarp();
     // thresholds: Kp-th smallest lane minimum, tightened by the seed
-    lane_min_thresholds(mins, thr_s[w], act, a.mode, a.k_raw, L);
+    lane_min_thresholds(mins, thr_s[w], ntp_s[w], act, a.mode, a.k_raw, L);
 
-    // ---- pass 2: collect candidates at or below the thresholds
+    // ---- pass 2: per candidate min_E (D_E - t'_E) < 0 marks a hit for some E;
+    //      the tile's marked candidates form a pool, processed in 32-lane rounds
+    int* pool = reinterpret_cast<int*>(wscr);
+    int bcount = 0;  // lane e: entries in dimension e's buffer
     for (int tile0 = 0; tile0 < L; tile0 += kTile) {
       const int p = tile0 + kRun * lane;
       const int zb = zi(p);
-      float2 D[kRun];
+      float2 D[kRun], Mn[kRun];
 #pragma unroll
       for (int c = 0; c < kRun; ++c) {
         D[c].x = (p + c == i) ? kInfF : 0.f;
         D[c].y = (p + kHalf + c == i) ? kInfF : 0.f;
+        Mn[c] = make_float2(kInfF, kInfF);
       }
 #pragma unroll 1
       for (int eb = 0; eb < nb; ++eb) {
@@ -432,43 +409,64 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
               D[c] = __ffma2_rn(df, df, D[c]);
             }
             if ((act >> e) & 1u) {
-              const float t = thr_s[w][e];
-              const bool has = tile_min(D) <= t;
-              if (__any_sync(CMB_FULL, has)) {
-                if (has) {
+              const float2 nt = ntp_s[w][e];
 #pragma unroll
-                  for (int c = 0; c < kRun; ++c) *reinterpret_cast<float2*>(wscr + lane * kScr + 2 * c) = D[c];
-                }
-                __syncwarp();
-                collect_hits(wscr + lane * kScr, has, list_of(wl, a.mode, e), wb + e * kCap, wc + 2 * e,
-                             &thr_s[w][e], p, kp_of(a.mode, a.k_raw, L, 1, e), a.diag);
+              for (int c = 0; c < kRun; ++c) {
+                const float2 u = __fadd2_rn(D[c], nt);
+                Mn[c].x = fminf(Mn[c].x, u.x);
+                Mn[c].y = fminf(Mn[c].y, u.y);
               }
             }
           }
         }
       }
-    }
-    __syncwarp();
-
-    // ---- end of row: sort the buffers into the lists
-#pragma unroll 1
-    for (int e = 0; e < eh; ++e) {
-      if (!((act >> e) & 1u)) continue;
-      int* cnt = wc + 2 * e;
-      const int bc = cnt[1];
-      if (bc > 0) {
-        const int lc = merge_buffer(list_of(wl, a.mode, e), wb + e * kCap, cnt[0], bc, kp_of(a.mode, a.k_raw, L, 1, e));
-        __syncwarp();
-        if (lane == 0) {
-          cnt[0] = lc;
-          cnt[1] = 0;
-        }
+      // pool of the tile in increasing j: every lane's first-run hits, then second-run hits
+      unsigned ha = 0, hb = 0;
+#pragma unroll
+      for (int c = 0; c < kRun; ++c) {
+        ha |= (Mn[c].x < 0.f ? 1u : 0u) << c;
+        hb |= (Mn[c].y < 0.f ? 1u : 0u) << c;
       }
+      const int na = __popc(ha), nb2 = __popc(hb);
+      int ia = na, ib = nb2;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int ua = __shfl_up_sync(CMB_FULL, ia, o);
+        const int ub = __shfl_up_sync(CMB_FULL, ib, o);
+        if (lane >= o) { ia += ua; ib += ub; }
+      }
+      const int tot_a = __shfl_sync(CMB_FULL, ia, 31);
+      const int total = tot_a + __shfl_sync(CMB_FULL, ib, 31);
+      int* da = pool + ia - na;
+      while (ha) {
+        const int c = __ffs(ha) - 1;
+        ha &= ha - 1;
+        *da++ = p + c;
+      }
+      int* db = pool + tot_a + ib - nb2;
+      while (hb) {
+        const int c = __ffs(hb) - 1;
+        hb &= hb - 1;
+        *db++ = p + kHalf + c;
+      }
+      __syncwarp();
+#ifdef CMB_KNN_STATS
+      if (a.diag && lane == 0) {
+        atomicAdd(a.diag + 3, (unsigned long long)total);
+        atomicAdd(a.diag + 4, (unsigned long long)((total + 31) / 32));
+      }
+#endif
+#pragma unroll 1
+      for (int q0 = 0; q0 < total; q0 += 32)
+        bcount = pool_round(pool + q0, min(32, total - q0), Z, nq_s[w], thr_s[w], wc, wl, wb, act, eh,
+                            a.mode, a.k_raw, L, bcount, a.diag ? a.diag + 5 : nullptr);
+      __syncwarp();
     }
+    if (lane < E_HI) wc[2 * lane + 1] = bcount;
     __syncwarp();
 
     // ---- certification, weights, records / predictions (v4 epilogue)
-    unsigned need = lane_finish<E_HI>(&a, wl, wb, wc, lib, i, act, M, emit);
+    unsigned need = lane_finish<E_HI>(&a, wl, wb, wc, lib, i, act, M, emit, true);
     __syncwarp();
 #pragma unroll 1
     while (need) {
@@ -483,11 +481,11 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
         acc4 += po.o * po.p;
       }
     }
-    prev_act = act;
     __syncwarp();
   }
 
   if (a.mode == KNN_EDIM) {
+    __syncthreads();  // every warp is done with its hit buffers
     if (lane < E_HI) {
       red[w][lane][0] = acc0;
       red[w][lane][1] = acc1;

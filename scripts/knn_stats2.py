@@ -12,8 +12,8 @@ X = P.mixed_dataset(N, 1450, seed=2105)
 est, _ = P.edim(X.T.astype(np.float64), 20, 1, 1)
 out = np.zeros(8, dtype=np.int64)
 nat.call("cmb_diagnostics", 0, nat.ptr(out), 8)
-print("edim rows", out[1], "hits/rowE %.2f calls/rowE %.2f slow/rowE %.4f fallback %d" % (out[3] / out[1], out[4] / out[1], out[5] / out[1], out[0]))
+print("edim rows", out[1], "pool/rowE %.2f rounds/rowE %.3f hits/rowE %.2f overflows/rowE %.4f fallback %d" % (out[3] / out[1], out[4] / out[1], out[5] / out[1], out[6] / out[1], out[0]))
 t0 = time.time()
 P.xmap(X.T, est, layout=P.LAYOUT_TGT_MAJOR, dtype=np.float32)
 nat.call("cmb_diagnostics", 0, nat.ptr(out), 8)
-print("xmap rows", out[1], "hits/rowE %.2f calls/rowE %.2f slow/rowE %.4f fallback %d" % (out[3] / out[1], out[4] / out[1], out[5] / out[1], out[0]), time.time() - t0)
+print("xmap rows", out[1], "pool/rowE %.2f rounds/rowE %.3f hits/rowE %.2f overflows/rowE %.4f fallback %d" % (out[3] / out[1], out[4] / out[1], out[5] / out[1], out[6] / out[1], out[0]), time.time() - t0)
