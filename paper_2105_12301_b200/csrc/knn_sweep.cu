@@ -42,8 +42,9 @@ cudaError_t launch_knn_sweep(const KnnArgs& a_in, cudaStream_t st) {
   // tile kernel (knn_tile.cuh) for unit lag and widths <= 20; the v4 sweep covers
   // tau > 1, wider sweeps, long RAW lists, and CMB_KNN_V4=1 (A/B runs)
   static const bool force_v4 = getenv("CMB_KNN_V4") && getenv("CMB_KNN_V4")[0] == '1';
+  // up to ~11k samples the pair-packed series + per-warp state fit one CTA's shared memory
   const bool tile_ok = !force_v4 && a.tau == 1 && W <= 20 && (a.mode != KNN_RAW || a.k_raw <= 30) &&
-                       (a.L + a.Tp) <= 6144;
+                       tile_smem_bytes_rt(W, a.L) + 12 * 1024 <= 227 * 1024;
   if (tile_ok) {
     a.x64_smem = 0;  // the tile kernel reads the float64 series (exact re-rank) through L1
     switch (W) {

@@ -507,6 +507,13 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
   }
 }
 
+// dynamic shared memory of the tile kernel for width W and library length L
+inline size_t tile_smem_bytes_rt(int W, int L) {
+  const int lt = list_off(W) < 32 ? 32 : list_off(W);
+  return sizeof(Entry) * kWarps * (size_t)(lt + W * kCap) + sizeof(float) * (kWarps * kScrWarp) +
+         sizeof(float2) * (size_t)z_len(L + kHalf + 32 + (W + kEB - 1) / kEB * kEB);
+}
+
 template <int W>
 size_t tile_smem_bytes(const KnnArgs& a) {
   const int Tfull = a.L + a.Tp;
