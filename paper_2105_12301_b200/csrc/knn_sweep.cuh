@@ -395,23 +395,25 @@ static __device__ __noinline__ unsigned lane_finish(const KnnArgs* __restrict__ 
     const int Kp = kp_of(a.mode, a.k_raw, a.L, a.tau, e);
     int lc = c[0];
     const int bc = c[1];
-    for (int b = 0; b < bc; ++b) {
-      const Entry x = Be[b];
-      const unsigned long long key = pack_key(x.d, x.j);
-      int pos;
-      if (lc == Kp) {
-        if (key >= pack_key(Le[Kp - 1].d, Le[Kp - 1].j)) continue;
-        pos = Kp - 1;
-      } else {
-        pos = lc++;
+    {
+      for (int b = 0; b < bc; ++b) {
+        const Entry x = Be[b];
+        const unsigned long long key = pack_key(x.d, x.j);
+        int pos;
+        if (lc == Kp) {
+          if (key >= pack_key(Le[Kp - 1].d, Le[Kp - 1].j)) continue;
+          pos = Kp - 1;
+        } else {
+          pos = lc++;
+        }
+        while (pos > 0) {
+          const Entry y = Le[pos - 1];
+          if (pack_key(y.d, y.j) < key) break;
+          Le[pos] = y;
+          --pos;
+        }
+        Le[pos] = x;
       }
-      while (pos > 0) {
-        const Entry y = Le[pos - 1];
-        if (pack_key(y.d, y.j) < key) break;
-        Le[pos] = y;
-        --pos;
-      }
-      Le[pos] = x;
     }
     c[0] = lc;
     c[1] = 0;
@@ -429,6 +431,7 @@ static __device__ __noinline__ unsigned lane_finish(const KnnArgs* __restrict__ 
           ok = A + sweep_err_bound(A, E, M) < B - sweep_err_bound(B, E, M);
         }
         if (ok) {
+          // scale: the smallest distance, or the first positive one (knn.py:194-199)
           float scale = sqrtf(Le[0].d);
           if (scale == 0.f) {
             scale = 1.f;
@@ -437,14 +440,21 @@ static __device__ __noinline__ unsigned lane_finish(const KnnArgs* __restrict__ 
               if (dq > 0.f) { scale = dq; break; }
             }
           }
+          // raw weights once (parked in the list entries, whose distances are not
+          // needed after this row), then normalised
+          const float inv = __fdividef(1.f, scale);
           float tot = 0.f;
-          for (int q = 0; q < k; ++q) tot += fmaxf(expf(-__fdividef(sqrtf(Le[q].d), scale)), FLT_MIN);
+          for (int q = 0; q < k; ++q) {
+            const float raw = fmaxf(expf(-sqrtf(Le[q].d) * inv), FLT_MIN);
+            Le[q].d = raw;
+            tot += raw;
+          }
+          const float itot = __fdividef(1.f, tot);
           const int kp4 = rec_kp4(k), kp8 = rec_kp8(k);
           uint8_t* rec = a.tab[E] + ((size_t)lib * nE + i) * (size_t)rec_bytes(k);
           float* wr = reinterpret_cast<float*>(rec);
           uint16_t* rr = reinterpret_cast<uint16_t*>(rec + 4 * kp4);
-          for (int q = 0; q < kp4; ++q)
-            wr[q] = (q < k) ? __fdividef(fmaxf(expf(-__fdividef(sqrtf(Le[q].d), scale)), FLT_MIN), tot) : 0.f;
+          for (int q = 0; q < kp4; ++q) wr[q] = (q < k) ? Le[q].d * itot : 0.f;
           for (int q = 0; q < kp8; ++q) rr[q] = (q < k) ? (uint16_t)(Le[q].j + e * a.tau) : (uint16_t)0;
           pending = false;
         }
@@ -481,45 +491,17 @@ __device__ __noinline__ PredObs epilogue_e(const KnnArgs* __restrict__ ap, Entry
   if (lane < Kp) en = Le[lane];
   const bool full = (Kp == nE - 1);  // every candidate was listed
 
-  if (a.mode == KNN_TABLE) {
-    // fp32 set certification: k-th and (k+1)-th separated beyond the error bounds
-    const float dk1 = __shfl_sync(CMB_FULL, en.d, k - 1);
-    const float dk = __shfl_sync(CMB_FULL, en.d, min(k, Kp - 1));
-    bool ok = full || (M == 0.0 && dk == 0.f);  // exact zeros: only identical vectors
-    if (!ok && isfinite(dk) && dk > 1e-30f) {
-      const double A = dk1, B = dk;
-      ok = A + sweep_err_bound(A, E, M) < B - sweep_err_bound(B, E, M);
-    }
-    if (ok) {
-      const float dist = (lane < k) ? sqrtf(en.d) : 0.f;
-      float scale = __shfl_sync(CMB_FULL, dist, 0);
-      if (scale == 0.f) {
-        const unsigned pm = __ballot_sync(CMB_FULL, lane < k && dist > 0.f);
-        scale = pm ? __shfl_sync(CMB_FULL, dist, __ffs(pm) - 1) : 1.f;
-      }
-      float raw = 0.f;
-      // fp32 table weights: fast division is well inside the fp32 storage precision
-      if (lane < k) raw = fmaxf(expf(-__fdividef(dist, scale)), FLT_MIN);
-      float tot = raw;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(CMB_FULL, tot, o);
-      const int kp4 = rec_kp4(k), kp8 = rec_kp8(k);
-      uint8_t* rec = a.tab[E] + ((size_t)lib * nE + i) * (size_t)rec_bytes(k);
-      if (lane < kp4) reinterpret_cast<float*>(rec)[lane] = (lane < k) ? __fdividef(raw, tot) : 0.f;
-      if (lane < kp8)
-        reinterpret_cast<uint16_t*>(rec + 4 * kp4)[lane] =
-            (lane < k) ? (uint16_t)(en.j + e * tau) : (uint16_t)0;
-      if (lane == 0 && a.diag) atomicAdd(a.diag + 1, 1ull);
-      return po;
-    }
-  }
-
+  // (the fp32 set certification already failed in lane_finish for every row
+  // that reaches this path)
   // fp64 path: exact distances of the listed candidates, re-sort, certify
   int jj = (lane < Kp) ? en.j : kNoJ;
   double dd = inf_d();
   if (lane < Kp && jj != kNoJ) dd = exact_sqdist_u<E_HI>(xp, i, jj, E, tau);
   sort_lanes(dd, jj, Kp);
-  const float t32 = __shfl_sync(CMB_FULL, en.d, Kp - 1);  // list threshold
+  // list threshold: its largest fp32 distance (the list is sorted, or a heap)
+  float t32 = (lane < Kp) ? en.d : -kInfF;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t32 = fmaxf(t32, __shfl_xor_sync(CMB_FULL, t32, o));
   bool ok = full || (M == 0.0 && t32 == 0.f);
   if (!ok) {
     const double dk = __shfl_sync(CMB_FULL, dd, k - 1);

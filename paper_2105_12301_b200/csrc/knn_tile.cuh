@@ -51,7 +51,7 @@ constexpr int kTile = 2 * kHalf;      // candidates per warp tile
 constexpr int kEB = 4;                // dimensions per unrolled block
 constexpr int kNW = kRun + kEB - 1;   // window pairs per block
 constexpr int kScr = kTC + 2;         // scratch row stride (floats): 8-byte aligned, conflict free
-constexpr int kScrWarp = 768;        // per-warp scratch: a tile's pool, or E_HI x 33 lane minima
+constexpr int kScrWarp = 800;        // per-warp scratch: carried + tile pool, or E_HI x 33 lane minima
 
 // pair-packed series: pair p = (x[p], x[p + kHalf]) at index zi(p), one pad pair per 4
 __device__ __forceinline__ int zi(int p) { return p + (p >> 2); }
@@ -384,6 +384,7 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
     //      the tile's marked candidates form a pool, processed in 32-lane rounds
     int* pool = reinterpret_cast<int*>(wscr);
     int bcount = 0;  // lane e: entries in dimension e's buffer
+    int carry = 0;   // pool entries (< 32) carried into the next tile's rounds
     for (int tile0 = 0; tile0 < L; tile0 += kTile) {
       const int p = tile0 + kRun * lane;
       const int zb = zi(p);
@@ -437,13 +438,13 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
       }
       const int tot_a = __shfl_sync(CMB_FULL, ia, 31);
       const int total = tot_a + __shfl_sync(CMB_FULL, ib, 31);
-      int* da = pool + ia - na;
+      int* da = pool + carry + ia - na;
       while (ha) {
         const int c = __ffs(ha) - 1;
         ha &= ha - 1;
         *da++ = p + c;
       }
-      int* db = pool + tot_a + ib - nb2;
+      int* db = pool + carry + tot_a + ib - nb2;
       while (hb) {
         const int c = __ffs(hb) - 1;
         hb &= hb - 1;
@@ -456,10 +457,20 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
         atomicAdd(a.diag + 4, (unsigned long long)((total + 31) / 32));
       }
 #endif
+      // full rounds now; a remainder waits for the next tile (the pool stays j-ordered)
+      const int avail = carry + total;
+      const bool last_tile = tile0 + kTile >= L;
+      int q0 = 0;
 #pragma unroll 1
-      for (int q0 = 0; q0 < total; q0 += 32)
-        bcount = pool_round(pool + q0, min(32, total - q0), Z, nq_s[w], thr_s[w], wc, wl, wb, act, eh,
+      for (; q0 + 32 <= avail || (last_tile && q0 < avail); q0 += 32)
+        bcount = pool_round(pool + q0, min(32, avail - q0), Z, nq_s[w], thr_s[w], wc, wl, wb, act, eh,
                             a.mode, a.k_raw, L, bcount, a.diag ? a.diag + 5 : nullptr);
+      carry = last_tile ? 0 : avail - q0;
+      if (carry) {
+        const int v = (lane < carry) ? pool[q0 + lane] : 0;
+        __syncwarp();
+        if (lane < carry) pool[lane] = v;
+      }
       __syncwarp();
     }
     if (lane < E_HI) wc[2 * lane + 1] = bcount;
