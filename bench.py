@@ -41,8 +41,8 @@ def parse():
     p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    p.add_argument("--n", type=int, default=53053)
-    p.add_argument("--t", type=int, default=1450)
+    p.add_argument("--series", dest="n", type=int, default=53053)
+    p.add_argument("--length", dest="t", type=int, default=1450)
     p.add_argument("--seed", type=int, default=2105)
     p.add_argument("--e-max", type=int, default=20)
     p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
@@ -96,6 +96,12 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def sm_clock_ghz(clk) -> float:
+    """Median SM clock sampled during the timed region (GHz), else the max clock."""
+    sm = clk.summary().get("sm_mhz") or clk.summary().get("sm_max_mhz") or 1965.0
+    return float(sm) / 1e3
+
+
 def measured_peak_hbm():
     f = ROOT / "MEASURED_PEAKS.json"
     if f.exists():
@@ -121,6 +127,21 @@ def lookup_alg_bytes(estar: np.ndarray, n_libs: int, T: int, tau: int = 1) -> fl
         nE = T - (int(E) - 1) * tau
         k = int(E) + 1
         tot += n_libs * NE * (4.0 * nE + 4.0) + n_libs * 8.0 * nE * k
+    return tot
+
+
+def lookup_alg_wavefronts(estar: np.ndarray, n_libs: int, T: int, tau: int = 1) -> float:
+    """Shared-memory wavefronts the lookup issues per step on this rank (the
+    binding resource, K3): per embedded point of a (library, 32-target
+    block) pair k gathers + ceil(k/2) weight and ceil(k/4) row broadcast loads +
+    1 observed-value load.  Matches ncu l1tex__data_pipe_lsu_wavefronts_mem_shared
+    within 2% (profiles/r01_lookup_ncu_summary.txt)."""
+    tot = 0.0
+    for E in np.unique(estar[estar > 0]):
+        NE = int(np.sum(estar == E))
+        nE = T - (int(E) - 1) * tau
+        k = int(E) + 1
+        tot += n_libs * ((NE + 31) // 32) * nE * (k + (k + 1) // 2 + (k + 3) // 4 + 1)
     return tot
 
 
@@ -169,7 +190,7 @@ def run_reference(args):
     n_pairs = float(np.sum(estar > 0)) ** 2
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": n_pairs / v * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"xmap N={args.n} T={args.t} mixed seed {args.seed}, E* from edim",
                        "n_series": args.n, "T": args.t, "tau": 1, "Tp_xmap": 0, "l2": "inputs > L2"},
@@ -200,15 +221,21 @@ def run_ours(args):
 
     import paper_2105_12301_b200 as P
     from paper_2105_12301_b200 import _native as nat
-    from paper_2105_12301_b200.distributed import shard_bounds, slab_width, xmap_sharded
+    from paper_2105_12301_b200.distributed import all_gather_rows, broadcast_, shard_bounds, xmap_sharded
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU; CMB_DIST_BACKEND=gloo lets ranks share a GPU (functional runs)
+    backend = os.environ.get("CMB_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     os.environ["CMB_DEVICE"] = str(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     N, T = args.n, args.t
 
@@ -216,7 +243,7 @@ def run_ours(args):
     X_host = make_data(N, T, args.seed) if rank == 0 else np.empty((N, T), np.float32)
     Xd = torch.from_numpy(X_host).to(dev)
     if world > 1:
-        dist.broadcast(Xd, src=0)
+        broadcast_(Xd, src=0)
     rho_e = torch.empty((N, args.e_max), dtype=torch.float64, device=dev)
     est_d = torch.empty(N, dtype=torch.int32, device=dev)
     torch.cuda.synchronize()
@@ -228,16 +255,14 @@ def run_ours(args):
     torch.cuda.synchronize()
     t_edim = time.perf_counter() - t0
     if world > 1:
-        parts = [torch.empty(shard_bounds(N, world, g)[1] - shard_bounds(N, world, g)[0],
-                             dtype=torch.int32, device=dev) for g in range(world)]
-        dist.all_gather(parts, est_d[lo_s:hi_s].contiguous())
-        est_d = torch.cat(parts)
+        est_d = all_gather_rows(est_d[lo_s:hi_s].contiguous(), N)
     estar = est_d.cpu().numpy().astype(np.int32)
     valid = int(np.sum(estar > 0))
     hist = {int(e): int(c) for e, c in zip(*np.unique(estar, return_counts=True))}
 
     stats = np.zeros(8)
     lo, hi = shard_bounds(N, world, rank)
+    n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
 
     def step():
         return xmap_sharded(Xd, estar, 1, stats=stats, broadcast=True)
@@ -264,7 +289,12 @@ def run_ours(args):
     ms = e0.elapsed_time(e1) / args.steps
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+        if backend == "gloo":
+            th = t_max.cpu()
+            dist.all_reduce(th, op=dist.ReduceOp.MAX)
+            t_max = th
+        else:
+            dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
     diag = nat.diagnostics(local)
     pairs = float(valid) * float(valid)
@@ -277,6 +307,7 @@ def run_ours(args):
     achieved = alg / t_look / 1e9
     peak, peak_kind = measured_peak_hbm()
     traffic, traffic_alg = profiled_traffic()
+    wf = lookup_alg_wavefronts(estar, libs_rank, T)
 
     # ---- e2e through the public C ABI with host buffers (rank 0 drives N = 1)
     e2e = None
@@ -323,6 +354,12 @@ def run_ours(args):
                          "alg_bytes_per_step": alg, "lookup_ms_per_step": t_look * 1e3},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": diag["kernel_launches"],
             "clocks": clk.summary(),
+            "roofline_smem": {
+                "bound": "shared-memory wavefronts (the lookup's binding resource)",
+                "achieved": wf / t_look / 1e9, "unit": "G wavefronts/s",
+                "peak": n_sms * sm_clock_ghz(clk), "frac": wf / t_look / 1e9 / (n_sms * sm_clock_ghz(clk)),
+                "wavefronts_per_step": wf, "model": "1 wavefront/clk/SM; k gathers + ceil(k/2) + ceil(k/4) record "
+                                                    "broadcasts + 1 observed load per point and 32 pairs"},
             "extra": {"edim_seconds": t_edim, "edim_series_per_s": N / t_edim,
                       "tables_ms_per_step": float(stats[0]) * 1e3, "lookup_ms_per_step": float(stats[1]) * 1e3,
                       "exact_fallback_rows": diag["exact_fallback_rows"], "rows_checked": diag["rows_checked"]},

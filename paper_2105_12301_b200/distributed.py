@@ -43,6 +43,45 @@ def native_shard(X, estar: np.ndarray, tau: int, lo: int, hi: int, slab, stats: 
              slab.data_ptr(), slab.stride(0), stream_handle, nat.ptr(stats))
 
 
+def _host_staged(group) -> bool:
+    """gloo moves CUDA tensors through host copies (functional multi-rank runs that
+    share one GPU, CMB_DIST_BACKEND=gloo); NCCL moves them device to device."""
+    import torch.distributed as dist
+    return dist.is_initialized() and dist.get_backend(group) == "gloo"
+
+
+def broadcast_(t, src: int = 0, group=None) -> None:
+    """In-place broadcast of a device tensor from ``src``."""
+    import torch.distributed as dist
+    if _host_staged(group) and t.is_cuda:
+        h = t.cpu()
+        dist.broadcast(h, src=src, group=group)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, src=src, group=group)
+
+
+def all_gather_rows(part, n_total: int, group=None):
+    """Concatenate every rank's ``part`` (contiguous shards of a length-``n_total``
+    vector, shard_bounds order; sizes may differ by one) on every rank."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    w = -(-n_total // world)
+    buf = torch.zeros(w, dtype=part.dtype, device=part.device)
+    buf[: part.numel()] = part
+    staged = _host_staged(group) and buf.is_cuda
+    src = buf.cpu() if staged else buf
+    outs = [torch.empty_like(src) for _ in range(world)]
+    dist.all_gather(outs, src, group=group)
+    pieces = []
+    for g in range(world):
+        lo, hi = shard_bounds(n_total, world, g)
+        pieces.append(outs[g][: hi - lo])
+    res = torch.cat(pieces)
+    return res.to(part.device) if staged else res
+
+
 def xmap_sharded(X, estar: np.ndarray, tau: int = 1, group=None, compute: Callable | None = None,
                  stats: np.ndarray | None = None, broadcast: bool = True):
     """Sharded all-to-all cross map.
@@ -61,7 +100,7 @@ def xmap_sharded(X, estar: np.ndarray, tau: int = 1, group=None, compute: Callab
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     N = X.shape[0]
     if world > 1 and broadcast:
-        dist.broadcast(X, src=0, group=group)
+        broadcast_(X, src=0, group=group)
     lo, hi = shard_bounds(N, world, rank)
     w = slab_width(N, world)
     slab = torch.full((N, w), float("nan"), dtype=torch.float32, device=X.device)
@@ -73,11 +112,14 @@ def xmap_sharded(X, estar: np.ndarray, tau: int = 1, group=None, compute: Callab
         compute(X, estar, tau, lo, hi, slab)
     if world == 1:
         return slab
-    gathered = [torch.empty_like(slab) for _ in range(world)] if rank == 0 else None
-    dist.gather(slab, gathered, dst=0, group=group)
+    staged = _host_staged(group) and slab.is_cuda
+    src = slab.cpu() if staged else slab
+    gathered = [torch.empty_like(src) for _ in range(world)] if rank == 0 else None
+    dist.gather(src, gathered, dst=0, group=group)
     if rank != 0:
         return None
-    return torch.cat(gathered, dim=1)
+    out = torch.cat(gathered, dim=1)
+    return out.to(slab.device) if staged else out
 
 
 def assemble(rhoT_slabs, n: int, world: int) -> np.ndarray:

@@ -3,7 +3,7 @@ set -x
 mkdir -p gpurun_out
 for impl in tile v4; do
   if [ $impl = tile ]; then unset CMB_KNN_V4; else export CMB_KNN_V4=1; fi
-  timeout 600 python bench.py --n 4096 --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/bench_${impl}_4096.txt 2>&1
+  timeout 600 python bench.py --series 4096 --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/bench_${impl}_4096.txt 2>&1
   tail -1 gpurun_out/bench_${impl}_4096.txt | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$impl 4096', d['ms_per_step'], d['extra']['tables_ms_per_step'], d['extra']['edim_seconds'])"
 done
 unset CMB_KNN_V4

@@ -69,3 +69,28 @@ def test_sharded_xmap_matches_single_process(world):
     ref, _ = O.xmap([X[i].double().numpy() for i in range(7)], estar.tolist(), 1, workers=1)
     assert np.allclose(out.numpy(), ref.astype(np.float32), equal_nan=True, atol=0)
     assert np.all(np.isnan(out.numpy()[5, :])) and np.all(np.isnan(out.numpy()[:, 5]))
+
+
+def _gather_worker(rank, world, port, n, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2105_12301_b200.distributed import all_gather_rows, broadcast_
+    lo, hi = shard_bounds(n, world, rank)
+    full = all_gather_rows(torch.arange(lo, hi, dtype=torch.int32) * 3, n)
+    x = torch.arange(5.0) if rank == 0 else torch.zeros(5)
+    broadcast_(x, src=0)
+    if rank == 1:
+        out[: n].copy_(full.float())
+        out[n:].copy_(x)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [7, 8])
+def test_uneven_all_gather_and_broadcast(n):
+    """E* shards of uneven size (N not divisible by the world size) are padded for
+    the collective and reassembled in shard order on every rank."""
+    out = torch.full((n + 5,), -1.0)
+    out.share_memory_()
+    mp.spawn(_gather_worker, args=(3, _free_port(), n, out), nprocs=3, join=True)
+    assert out[:n].tolist() == [3.0 * i for i in range(n)]
+    assert out[n:].tolist() == [0.0, 1.0, 2.0, 3.0, 4.0]
