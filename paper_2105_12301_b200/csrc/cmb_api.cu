@@ -301,7 +301,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   size_t tab_off[CMB_SWEEP_MAX_E + 2] = {0};
   for (int g = 0; g < la.ngroups; ++g) {
     const int e = la.g_E[g];
-    per_lib += (size_t)(T - (int64_t)(e - 1) * tau) * rec_bytes(e + 1);
+    per_lib += rec_lib_stride(e + 1, T - (int64_t)(e - 1) * tau);
   }
   const int LS = 64;
   const size_t budget = (size_t)6 << 30;
@@ -314,7 +314,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     for (int g = 0; g < la.ngroups; ++g) {
       const int e = la.g_E[g];
       tab_off[e] = o;
-      o += (size_t)C * (T - (int64_t)(e - 1) * tau) * rec_bytes(e + 1);
+      o += (size_t)C * rec_lib_stride(e + 1, T - (int64_t)(e - 1) * tau);
     }
   }
 

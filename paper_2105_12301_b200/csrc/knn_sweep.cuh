@@ -450,12 +450,11 @@ static __device__ __noinline__ unsigned lane_finish(const KnnArgs* __restrict__ 
             tot += raw;
           }
           const float itot = __fdividef(1.f, tot);
-          const int kp4 = rec_kp4(k), kp8 = rec_kp8(k);
-          uint8_t* rec = a.tab[E] + ((size_t)lib * nE + i) * (size_t)rec_bytes(k);
+          uint8_t* rec = a.tab[E] + (size_t)lib * rec_lib_stride(k, nE) + (size_t)i * rec_bytes(k);
           float* wr = reinterpret_cast<float*>(rec);
-          uint16_t* rr = reinterpret_cast<uint16_t*>(rec + 4 * kp4);
-          for (int q = 0; q < kp4; ++q) wr[q] = (q < k) ? Le[q].d * itot : 0.f;
-          for (int q = 0; q < kp8; ++q) rr[q] = (q < k) ? (uint16_t)(Le[q].j + e * a.tau) : (uint16_t)0;
+          uint16_t* rr = reinterpret_cast<uint16_t*>(rec + rec_row_off(k));
+          for (int q = 0; q < rec_nw(k); ++q) wr[q] = (q < k) ? Le[q].d * itot : 0.f;
+          for (int q = 0; q < rec_nr(k); ++q) rr[q] = (q < k) ? (uint16_t)(Le[q].j + e * a.tau) : (uint16_t)0;
           pending = false;
         }
       }
@@ -528,11 +527,10 @@ __device__ __noinline__ PredObs epilogue_e(const KnnArgs* __restrict__ ap, Entry
   const double wgt = raw / warp_sum_d(raw);
 
   if (a.mode == KNN_TABLE) {
-    const int kp4 = rec_kp4(k), kp8 = rec_kp8(k);
-    uint8_t* rec = a.tab[E] + ((size_t)lib * nE + i) * (size_t)rec_bytes(k);
-    if (lane < kp4) reinterpret_cast<float*>(rec)[lane] = (lane < k) ? (float)wgt : 0.f;
-    if (lane < kp8)
-      reinterpret_cast<uint16_t*>(rec + 4 * kp4)[lane] = (lane < k) ? (uint16_t)(jj + e * tau) : (uint16_t)0;
+    uint8_t* rec = a.tab[E] + (size_t)lib * rec_lib_stride(k, nE) + (size_t)i * rec_bytes(k);
+    if (lane < rec_nw(k)) reinterpret_cast<float*>(rec)[lane] = (lane < k) ? (float)wgt : 0.f;
+    if (lane < rec_nr(k))
+      reinterpret_cast<uint16_t*>(rec + rec_row_off(k))[lane] = (lane < k) ? (uint16_t)(jj + e * tau) : (uint16_t)0;
   } else if (a.mode == KNN_EDIM) {
     // prediction of x[i + (E-1)tau + Tp] from the neighbours' futures
     const int off = e * tau + a.Tp;

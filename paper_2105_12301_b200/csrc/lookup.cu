@@ -80,6 +80,7 @@ __device__ __forceinline__ void lds_v2(uint32_t addr, uint32_t& x, uint32_t& y) 
 
 struct WarpStream {
   const uint8_t* base;  // table of the warp's first library
+  size_t stride;        // bytes per library table (16-byte multiple)
   int n;                // records per library
   int R;                // record bytes
   int RS;               // records per stage
@@ -91,8 +92,9 @@ __device__ __forceinline__ void issue_stage(const WarpStream& ws, int q, uint8_t
   const int l = q / ws.nst, s = q - l * ws.nst;
   const int r0 = s * ws.RS;
   const int nrec = min(ws.RS, ws.n - r0);
-  const uint32_t bytes = (uint32_t)(nrec * ws.R);
-  const uint8_t* src = ws.base + ((size_t)l * ws.n + r0) * ws.R;
+  // bulk copies move 16-byte multiples; a library's table is padded to 16 bytes
+  const uint32_t bytes = (uint32_t)((nrec * ws.R + 15) & ~15);
+  const uint8_t* src = ws.base + (size_t)l * ws.stride + (size_t)r0 * ws.R;
   mbar_expect_tx(bar, bytes);
   bulk_g2s(slot, src, bytes, bar);
 }
@@ -103,14 +105,15 @@ template <int K, bool RESIDENT>
 __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float* __restrict__ tgt,
                                                uint8_t* ring, uint64_t* bars, uint32_t& qglob,
                                                int E, int lib0, int nl, int slot_base) {
-  constexpr int KP4 = rec_kp4(K), KP8 = rec_kp8(K);
-  constexpr int R = 4 * KP4 + 2 * KP8;
+  constexpr int R = rec_bytes(K);
+  constexpr int RO = rec_row_off(K);
   const int64_t stride = RESIDENT ? 32 : a.ldy;
   const int lane = lane_id();
   const int n = a.T - (E - 1) * a.tau;
   const int off = (E - 1) * a.tau;
   WarpStream ws;
-  ws.base = a.tab[E] + (size_t)lib0 * n * R;
+  ws.stride = rec_lib_stride(K, n);
+  ws.base = a.tab[E] + (size_t)lib0 * ws.stride;
   ws.n = n;
   ws.R = R;
   ws.RS = a.stage_bytes / R;
@@ -151,13 +154,43 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
       // broadcast 16-byte load costs two, so keep the compiler from merging)
       float wv[2 * ((K + 1) / 2)];
       uint32_t rv[2 * ((K + 3) / 4)];
-#pragma unroll
-      for (int c = 0; c < (K + 1) / 2; ++c) lds_v2(rec + 8 * c, wv[2 * c], wv[2 * c + 1]);
-#pragma unroll
-      for (int c = 0; c < (K + 3) / 4; ++c) lds_v2(rec + 4 * KP4 + 8 * c, rv[2 * c], rv[2 * c + 1]);
       float o, p = 0.f;
-      if (RESIDENT) {
-        // 32-bit shared addresses: byte offset of sample row s is s << 7
+      if constexpr (K == 2) {
+        // [w0][r0 r1]: the last weight is 1 - w0, p = y1 + w0 (y0 - y1)
+        uint32_t u0;
+        lds_v2(rec, u0, rv[0]);
+        wv[0] = __uint_as_float(u0);
+      } else {
+#pragma unroll
+        // weights used: k (explicit) or k - 1 (implicit last weight)
+        for (int c = 0; c < ((rec_implicit(K) ? K - 1 : K) + 1) / 2; ++c)
+          lds_v2(rec + 8 * c, wv[2 * c], wv[2 * c + 1]);
+#pragma unroll
+        for (int c = 0; c < (K + 3) / 4; ++c) lds_v2(rec + RO + 8 * c, rv[2 * c], rv[2 * c + 1]);
+      }
+      if constexpr (rec_implicit(K)) {
+        // k - 1 stored weights, the last implied: p = y_last + sum w_q (y_q - y_last)
+        float yv[K];
+        if (RESIDENT) {
+          // 32-bit shared addresses: byte offset of sample row s is s << 7
+          o = lds_f32(tbase + ((uint32_t)(off + r0 + r) << 7));
+#pragma unroll
+          for (int kk = 0; kk < K; ++kk) {
+            const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+            yv[kk] = lds_f32(tbase + (row << 7));
+          }
+        } else {
+          o = tcol[(int64_t)(off + r0 + r) * stride];
+#pragma unroll
+          for (int kk = 0; kk < K; ++kk) {
+            const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+            yv[kk] = tcol[(int64_t)row * stride];
+          }
+        }
+        p = yv[K - 1];
+#pragma unroll
+        for (int kk = 0; kk < K - 1; ++kk) p = __fmaf_rn(wv[kk], __fsub_rn(yv[kk], yv[K - 1]), p);
+      } else if (RESIDENT) {
         o = lds_f32(tbase + ((uint32_t)(off + r0 + r) << 7));
 #pragma unroll
         for (int kk = 0; kk < K; ++kk) {
