@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -66,6 +67,7 @@ enum BufId {
 struct Ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // D2H overlap of the host-buffer cross map
   std::mutex mu;
   DevBuf buf[B_NBUF];
   bool ready = false;
@@ -222,9 +224,14 @@ struct XmapStats {
   double tables = 0, distinct = 0, pairs = 0;
 };
 
+// on_chunk(col_lo, col_hi): called after the lookup of each library chunk has
+// been enqueued on st, with the rho_T column range that is final once st reaches
+// that point (the host-buffer entry point overlaps its D2H copy with later chunks)
+using ChunkFn = std::function<int(int64_t, int64_t)>;
+
 static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64_t T, int64_t ld,
                      const int32_t* estar, int tau, int64_t lib_begin, int64_t lib_end, float* rhoT,
-                     int64_t ldr, XmapStats* stats) {
+                     int64_t ldr, XmapStats* stats, const ChunkFn& on_chunk = nullptr) {
   CMB_PARAM(tau >= 1, "tau must be >= 1, got %d", tau);
   CMB_PARAM(lib_begin >= 0 && lib_begin <= lib_end && lib_end <= N, "bad library range [%lld, %lld)",
             (long long)lib_begin, (long long)lib_end);
@@ -267,7 +274,10 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     }
   const int64_t ncols = lib_end - lib_begin;
   CMB_CUDA(launch_fill_nan(rhoT, N, ncols, ldr, st));
-  if (la.ngroups == 0 || lib_rows.empty()) return CMB_OK;
+  if (la.ngroups == 0 || lib_rows.empty()) {
+    if (on_chunk) CMB_TRY(on_chunk(0, ncols));
+    return CMB_OK;
+  }
   const int stage = lookup_stage_bytes((int)T, max_rec);
 
   // ---- device staging
@@ -372,6 +382,12 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->dev);
     CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(items, dev_sms), st));
+    if (on_chunk) {
+      // columns [first column of this chunk (0 for the first), first column of the next chunk)
+      const int64_t col_lo = (c0 == 0) ? 0 : lib_rows[c0] - lib_begin;
+      const int64_t col_hi = (c0 + nc < (int64_t)lib_rows.size()) ? lib_rows[c0 + nc] - lib_begin : ncols;
+      CMB_TRY(on_chunk(col_lo, col_hi));
+    }
     CMB_CUDA(cudaEventRecord(ev[2], st));
     CMB_CUDA(cudaEventSynchronize(ev[2]));
     float a_ms = 0, b_ms = 0;
@@ -670,12 +686,36 @@ int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* est
   CMB_CUDA(cudaEventRecord(e0, st));
   CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X32].p, X, sizeof(float) * N * len, cudaMemcpyHostToDevice, st));
   XmapStats s;
-  CMB_TRY(xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
-                    ctx->buf[B_RHOT].as<float>(), ldr, &s));
   if (layout == CMB_LAYOUT_TGT_MAJOR) {
-    CMB_CUDA(cudaMemcpy2DAsync(rho_out, sizeof(float) * N, ctx->buf[B_RHOT].p, sizeof(float) * ldr,
-                               sizeof(float) * N, N, cudaMemcpyDeviceToHost, st));
+    // target-major output: copy each chunk's finished columns to the host on a
+    // second stream while the next chunks compute
+    if (!ctx->copy_stream) CMB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> done;
+    const float* rt = ctx->buf[B_RHOT].as<float>();
+    auto on_chunk = [&](int64_t lo, int64_t hi) -> int {
+      if (hi <= lo) return CMB_OK;
+      cudaEvent_t ev;
+      CMB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      done.push_back(ev);
+      CMB_CUDA(cudaEventRecord(ev, st));
+      CMB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev, 0));
+      CMB_CUDA(cudaMemcpy2DAsync(rho_out + lo, sizeof(float) * N, rt + lo, sizeof(float) * ldr,
+                                 sizeof(float) * (hi - lo), N, cudaMemcpyDeviceToHost, ctx->copy_stream));
+      return CMB_OK;
+    };
+    const int rc = xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
+                             ctx->buf[B_RHOT].as<float>(), ldr, &s, on_chunk);
+    cudaEvent_t copied;
+    CMB_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    CMB_CUDA(cudaEventRecord(copied, ctx->copy_stream));
+    CMB_CUDA(cudaStreamWaitEvent(st, copied, 0));
+    CMB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    cudaEventDestroy(copied);
+    for (auto ev : done) cudaEventDestroy(ev);
+    if (rc) return rc;
   } else {
+    CMB_TRY(xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
+                      ctx->buf[B_RHOT].as<float>(), ldr, &s));
     CMB_CUDA(ctx->buf[B_RHO].ensure(sizeof(float) * N * ldr));
     CMB_CUDA(launch_transpose_f32(ctx->buf[B_RHOT].as<float>(), N, N, ldr, ctx->buf[B_RHO].as<float>(), ldr, st));
     CMB_CUDA(cudaMemcpy2DAsync(rho_out, sizeof(float) * N, ctx->buf[B_RHO].p, sizeof(float) * ldr,
