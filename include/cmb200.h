@@ -130,6 +130,35 @@ int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E,
                         const int32_t* sizes, int n_sizes, int samples, const int32_t* pts,
                         double* rho_out);
 
+/* ---- data formats either side of the path ---------- */
+
+/* write_skill_matrix (pkg/src/crossmap/io.py:70-78), the cell rows: text of
+ * rows [row0, row0 + nrows) of an n x n skill matrix -- per row the
+ * pre-rendered CSV name field names[name_off[r] .. name_off[r+1]) (name_off
+ * holds n + 1 entries), then for each cell ',' and f"{v:.6f}" of the float64
+ * value (float32 input is widened exactly) or "NA" when not finite, then
+ * "\r\n" (csv.writer's terminator) -- formatted on the GPU, byte-identical
+ * to the reference.  rho points to row row0 (row-major, leading dimension ld),
+ * in device memory when rho_on_device, else host memory; is_f32 selects float.
+ * Text goes to out (host, capacity out_cap bytes), its length to *out_len;
+ * CMB_ERR_PARAM if it does not fit or a finite |v| >= 1e9 (skill is in
+ * [-1, 1]).                                                                  */
+int cmb_format_skill_csv(int dev, const void* rho, int rho_on_device, int is_f32, int64_t n,
+                         int64_t ld, int64_t row0, int64_t nrows, const char* names,
+                         const int64_t* name_off, char* out, int64_t out_cap, int64_t* out_len);
+
+/* load_csv / read_skill_matrix (io.py:25-61, 81-110), numeric body: parse the
+ * lines of buf (after the header) into out[row][ncols] with std::from_chars
+ * (correctly rounded, like Python float()); label_col: the first cell of a row
+ * is a label, its byte span goes to labels[2 r], labels[2 r + 1]; allow_na:
+ * the cell "NA" is NaN; check_finite: inf/nan are rejected.  Host only (no
+ * device needed).  Returns 0 and *nrows, or 1 when the text is outside this
+ * grammar or invalid -- the caller then runs the reference algorithm, which
+ * raises the reference's exact CsvFormatError.                              */
+int cmb_parse_numeric_csv(const char* buf, int64_t len, int64_t ncols, int label_col, int allow_na,
+                          int check_finite, double* out, int64_t cap_rows, int64_t* nrows,
+                          int64_t* labels);
+
 #ifdef __cplusplus
 }
 #endif

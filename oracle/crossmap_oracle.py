@@ -446,3 +446,19 @@ def ccm_convergence(lib_series, tgt_series, E: int, tau: int, sizes, samples: in
     with np.errstate(all="ignore"):
         means = np.array([np.nanmean(row) if np.any(np.isfinite(row)) else np.nan for row in per])
     return means, per
+
+
+# ---------------------------------------------------------------- data formats
+def skill_matrix_csv_bytes(names, rho) -> bytes:
+    """write_skill_matrix (pkg/src/crossmap/io.py:66-78) restated: csv.writer rows
+    ["", *names] then [name, *cells], cell = f"{v:.6f}" or "NA" when not finite,
+    "\\r\\n" terminators.  Pinned by tests/golden/io_cases.json (reference output)."""
+    import csv
+    import io
+    import math
+    buf = io.StringIO(newline="")
+    w = csv.writer(buf)
+    w.writerow([""] + list(names))
+    for i, name in enumerate(names):
+        w.writerow([name] + ["NA" if not math.isfinite(float(v)) else f"{float(v):.6f}" for v in rho[i]])
+    return buf.getvalue().encode("utf-8")

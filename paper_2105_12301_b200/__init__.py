@@ -54,6 +54,8 @@ def edim(values, E_max: int = DEFAULT_E_MAX, tau: int = 1, Tp: int = 1):
 
 from . import convergence  # noqa: E402
 from .convergence import Convergence, ccm, ccm_sweep  # noqa: E402  (kEDM ``ccm``)
+from .io import (load_csv, read_skill_matrix, read_skill_matrix_npz,  # noqa: E402
+                 write_skill_matrix, write_skill_matrix_device, write_skill_matrix_npz)
 
 
 __all__ = [
@@ -66,4 +68,6 @@ __all__ = [
     "logistic_map", "lookup_batch", "mixed_dataset", "normalize_to_weights", "optimal_embedding",
     "oracle_knn", "pairwise_distances", "partial_sort_topk", "pearson_stream", "simplex",
     "simplex_self_predict", "skill_curves", "uniform_noise", "valid_count", "xmap",
+    "load_csv", "read_skill_matrix", "read_skill_matrix_npz", "write_skill_matrix",
+    "write_skill_matrix_device", "write_skill_matrix_npz",
 ]

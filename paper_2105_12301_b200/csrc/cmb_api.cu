@@ -61,7 +61,7 @@ struct DevBuf {
 enum BufId {
   B_X64, B_X32, B_ERR, B_MEAN, B_Y, B_SLOT_TGT, B_SLOT_E, B_OBS_S, B_OBS_SS, B_OBS_C, B_LIBROWS,
   B_LIBCOL, B_TAB, B_COUNTER, B_RHOT, B_RHO, B_PART, B_LAST, B_LMEAN, B_A, B_B, B_C, B_D, B_E,
-  B_DIAG, B_EST, B_NBUF
+  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_NBUF
 };
 
 struct Ctx {
@@ -805,6 +805,51 @@ int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E,
               host_rho[((size_t)s * samples + q) * M + m];
   }
   return CMB_OK;
+}
+
+// ---------------------------------------------------------------- data formats
+int cmb_format_skill_csv(int dev, const void* rho, int rho_on_device, int is_f32, int64_t n,
+                         int64_t ld, int64_t row0, int64_t nrows, const char* names,
+                         const int64_t* name_off, char* out, int64_t out_cap, int64_t* out_len) {
+  CMB_PARAM(n >= 1 && ld >= n && row0 >= 0 && nrows >= 0 && row0 + nrows <= n, "bad skill-matrix block");
+  CMB_PARAM(rho && names && name_off && out && out_len, "null buffer");
+  CMB_CTX(dev);
+  const size_t esz = is_f32 ? 4 : 8;
+  const void* src = rho;
+  if (!rho_on_device && nrows > 0) {
+    CMB_CUDA(ctx->buf[B_FMT_RHO].ensure(esz * nrows * ld));
+    CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_FMT_RHO].p, rho, esz * ((nrows - 1) * ld + n), cudaMemcpyHostToDevice, st));
+    src = ctx->buf[B_FMT_RHO].p;
+  }
+  const int64_t nbytes = name_off[n];
+  CMB_CUDA(ctx->buf[B_FMT_NAMES].ensure(nbytes + 1));
+  CMB_CUDA(ctx->buf[B_FMT_OFF].ensure(8 * (n + 1)));
+  CMB_CUDA(ctx->buf[B_FMT_LEN].ensure(8 * (nrows + 1) + 8));
+  CMB_CUDA(ctx->buf[B_FMT_ROWOFF].ensure(8 * (nrows + 1)));
+  CMB_CUDA(ctx->buf[B_FMT_OUT].ensure(out_cap + 1));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_FMT_NAMES].p, names, nbytes, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_FMT_OFF].p, name_off, 8 * (n + 1), cudaMemcpyHostToDevice, st));
+  std::vector<int64_t> row_off(nrows + 1);
+  bool oor = false;
+  int64_t len = 0;
+  int64_t* lens = ctx->buf[B_FMT_LEN].as<int64_t>();
+  CMB_CUDA(format_skill_rows(src, is_f32 != 0, n, ld, row0, nrows, ctx->buf[B_FMT_NAMES].as<char>(),
+                             ctx->buf[B_FMT_OFF].as<int64_t>(), lens, ctx->buf[B_FMT_ROWOFF].as<int64_t>(),
+                             row_off.data(), reinterpret_cast<int*>(lens + nrows + 1), &oor,
+                             ctx->buf[B_FMT_OUT].as<char>(), out_cap, &len, st));
+  CMB_PARAM(!oor, "skill value outside the formatter's range (|v| >= 1e9)");
+  CMB_PARAM(len <= out_cap, "text of %lld bytes exceeds the %lld-byte buffer", (long long)len, (long long)out_cap);
+  CMB_CUDA(cudaMemcpyAsync(out, ctx->buf[B_FMT_OUT].p, len, cudaMemcpyDeviceToHost, st));
+  CMB_CUDA(cudaStreamSynchronize(st));
+  *out_len = len;
+  return CMB_OK;
+}
+
+int cmb_parse_numeric_csv(const char* buf, int64_t len, int64_t ncols, int label_col, int allow_na,
+                          int check_finite, double* out, int64_t cap_rows, int64_t* nrows,
+                          int64_t* labels) {
+  if (!buf || len < 0 || ncols < 1 || !out || !nrows || (label_col && !labels)) return 1;
+  return parse_numeric_csv(buf, len, ncols, label_col, allow_na, check_finite, out, cap_rows, nrows, labels);
 }
 
 }  // extern "C"

@@ -109,4 +109,13 @@ cudaError_t launch_restricted_tables(const double* x, int n, int E, int tau, int
 cudaError_t launch_transpose_f32(const float* src, int64_t rows, int64_t cols, int64_t lds,
                                  float* dst, int64_t ldd, cudaStream_t st);
 
+// ------------------------------------------------------------------ data formats (io.cu)
+cudaError_t format_skill_rows(const void* rho_dev, bool f32, int64_t n, int64_t ld, int64_t row0,
+                              int64_t nrows, const char* names_dev, const int64_t* name_off_dev,
+                              int64_t* row_len_dev, int64_t* row_off_dev, int64_t* row_off_host,
+                              int* range_err_dev, bool* out_of_range, char* out_dev, int64_t out_cap,
+                              int64_t* out_len, cudaStream_t st);
+int parse_numeric_csv(const char* buf, int64_t len, int64_t ncols, int label_col, int allow_na,
+                      int check_finite, double* out, int64_t cap_rows, int64_t* nrows, int64_t* labels);
+
 }  // namespace cmb
