@@ -56,6 +56,7 @@ from . import convergence  # noqa: E402
 from .convergence import Convergence, ccm, ccm_sweep  # noqa: E402  (kEDM ``ccm``)
 from .io import (load_csv, read_skill_matrix, read_skill_matrix_npz,  # noqa: E402
                  write_skill_matrix, write_skill_matrix_device, write_skill_matrix_npz)
+from .bench import BenchRow, run_bench  # noqa: E402  (kernel micro-benchmarks, bench.py)
 
 
 __all__ = [
@@ -69,5 +70,5 @@ __all__ = [
     "oracle_knn", "pairwise_distances", "partial_sort_topk", "pearson_stream", "simplex",
     "simplex_self_predict", "skill_curves", "uniform_noise", "valid_count", "xmap",
     "load_csv", "read_skill_matrix", "read_skill_matrix_npz", "write_skill_matrix",
-    "write_skill_matrix_device", "write_skill_matrix_npz",
+    "write_skill_matrix_device", "write_skill_matrix_npz", "BenchRow", "run_bench",
 ]
