@@ -7,6 +7,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <memory>
@@ -61,7 +62,7 @@ struct DevBuf {
 enum BufId {
   B_X64, B_X32, B_ERR, B_MEAN, B_Y, B_SLOT_TGT, B_SLOT_E, B_OBS_S, B_OBS_SS, B_OBS_C, B_LIBROWS,
   B_LIBCOL, B_TAB, B_COUNTER, B_RHOT, B_RHO, B_PART, B_LAST, B_LMEAN, B_A, B_B, B_C, B_D, B_E,
-  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_NBUF
+  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_YH, B_NBUF
 };
 
 struct Ctx {
@@ -249,13 +250,17 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   memset(&la, 0, sizeof(la));
   uint32_t need = 0;
   int e_hi = 0, max_rec = 0;
+  // opt-in fp16 target blocks (64 targets per block, lookup.cu warp_libraries_h16)
+  const char* h16_env = getenv("CMB_LOOKUP_FP16");
+  const bool want_h16 = h16_env && h16_env[0] == '1';
+  const int blk_sz = want_h16 ? 64 : 32;
   for (int e = 1; e <= CMB_SWEEP_MAX_E; ++e) {
     if (by_e[e].empty()) continue;
     CMB_TRY(check_valid_count(T, e, tau));
     const int g = la.ngroups++;
     la.g_E[g] = e;
     la.g_blk0[g] = (int)(slot_tgt.size() / 32);
-    const size_t padded = (by_e[e].size() + 31) / 32 * 32;
+    const size_t padded = (by_e[e].size() + blk_sz - 1) / blk_sz * blk_sz;
     la.g_nblk[g] = (int)(padded / 32);
     for (size_t q = 0; q < padded; ++q) {
       slot_tgt.push_back(q < by_e[e].size() ? by_e[e][q] : -1);
@@ -301,9 +306,21 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   CMB_CUDA(launch_series_stats(X, N, T, ld, ctx->buf[B_MEAN].as<double>(), st));
   CMB_CUDA(launch_build_targets(X, ld, ctx->buf[B_MEAN].as<double>(), ctx->buf[B_SLOT_TGT].as<int32_t>(),
                                 slots, (int)T, ctx->buf[B_Y].as<float>(), ldy, st));
-  CMB_CUDA(launch_obs_moments(ctx->buf[B_Y].as<float>(), ldy, (int)T, tau, ctx->buf[B_SLOT_E].as<int32_t>(),
-                              slots, ctx->buf[B_OBS_S].as<double>(), ctx->buf[B_OBS_SS].as<double>(),
-                              ctx->buf[B_OBS_C].as<uint8_t>(), st));
+  const bool h16 = want_h16 && stage != kNonResidentStage;
+  if (h16) {
+    for (int g = 0; g < la.ngroups; ++g) {  // blocks of 64 slots
+      la.g_blk0[g] /= 2;
+      la.g_nblk[g] /= 2;
+    }
+    CMB_CUDA(ctx->buf[B_YH].ensure(2 * T * ldy));
+    CMB_CUDA(launch_targets_to_half(ctx->buf[B_Y].as<float>(), ldy, (int)T, tau, ctx->buf[B_SLOT_E].as<int32_t>(),
+                                    slots, ctx->buf[B_YH].p, ctx->buf[B_OBS_S].as<double>(),
+                                    ctx->buf[B_OBS_SS].as<double>(), ctx->buf[B_OBS_C].as<uint8_t>(), st));
+  } else {
+    CMB_CUDA(launch_obs_moments(ctx->buf[B_Y].as<float>(), ldy, (int)T, tau, ctx->buf[B_SLOT_E].as<int32_t>(),
+                                slots, ctx->buf[B_OBS_S].as<double>(), ctx->buf[B_OBS_SS].as<double>(),
+                                ctx->buf[B_OBS_C].as<uint8_t>(), st));
+  }
   CMB_CUDA(launch_promote(X, N, T, ld, ctx->buf[B_X64].as<double>(), st));
 
   // ---- library chunks: tables for every needed E, then the lookup
@@ -354,7 +371,8 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     CMB_CUDA(launch_knn_sweep(a, st));
     CMB_CUDA(cudaEventRecord(ev[1], st));
 
-    la.Y = ctx->buf[B_Y].as<float>();
+    la.Y = h16 ? reinterpret_cast<const float*>(ctx->buf[B_YH].p) : ctx->buf[B_Y].as<float>();
+    la.h16 = h16 ? 1 : 0;
     la.ldy = ldy;
     la.T = (int)T;
     la.tau = tau;

@@ -25,6 +25,8 @@
 #include "cmb_common.cuh"
 #include "kernels.cuh"
 
+#include <cuda_fp16.h>
+
 namespace cmb {
 
 namespace {
@@ -69,6 +71,18 @@ __device__ __forceinline__ float lds_f32(uint32_t addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ float2 h2f2(uint32_t u) {
+  __half2 h;
+  memcpy(&h, &u, 4);
+  return __half22float2(h);
 }
 
 __device__ __forceinline__ void lds_v2(uint32_t addr, float& x, float& y) {
@@ -229,7 +243,127 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
   qglob += ws.total;
 }
 
-template <bool RESIDENT>
+// fp16-target variant (opt-in, CMB_LOOKUP_FP16=1): the resident block holds 64
+// targets as fp16 scaled to [-1, 1] -- the same 128 bytes per sample row -- and
+// lane l owns targets 2l and 2l + 1, so every shared-memory wavefront (gathers,
+// record broadcasts, observed values) serves 64 pairs instead of 32.  Values are
+// widened to fp32 and accumulated with packed FFMA2; rho as in the fp32 path.
+template <int K>
+__device__ __forceinline__ void warp_libraries_h16(const LookupArgs& a, const uint8_t* tgt,
+                                                   uint8_t* ring, uint64_t* bars, uint32_t& qglob,
+                                                   int E, int lib0, int nl, int slot_base) {
+  constexpr int R = rec_bytes(K);
+  constexpr int RO = rec_row_off(K);
+  const int lane = lane_id();
+  const int n = a.T - (E - 1) * a.tau;
+  const int off = (E - 1) * a.tau;
+  WarpStream ws;
+  ws.stride = rec_lib_stride(K, n);
+  ws.base = a.tab[E] + (size_t)lib0 * ws.stride;
+  ws.n = n;
+  ws.R = R;
+  ws.RS = a.stage_bytes / R;
+  ws.nst = (n + ws.RS - 1) / ws.RS;
+  ws.total = nl * ws.nst;
+
+  int tid[2];
+  double So[2], Soo[2];
+  bool ocst[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int slot = slot_base + 2 * lane + h;
+    tid[h] = a.slot_tgt[slot];
+    So[h] = a.obs_s[slot];
+    Soo[h] = a.obs_ss[slot];
+    ocst[h] = a.obs_const[slot] != 0;
+  }
+  const uint32_t tbase = smem_u32(tgt) + 4 * lane;
+
+  if (lane == 0) {
+    for (int q = 0; q < 2 && q < ws.total; ++q) {
+      const uint32_t g = qglob + q;
+      issue_stage(ws, q, ring + (g & 1) * a.stage_bytes, bars + (g & 1));
+    }
+  }
+  __syncwarp();
+
+  double Sp0 = 0, Sp1 = 0, Spp0 = 0, Spp1 = 0, Sop0 = 0, Sop1 = 0;
+  for (int q = 0; q < ws.total; ++q) {
+    const uint32_t g = qglob + q;
+    uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
+    mbar_wait(bars + (g & 1), (g >> 1) & 1);
+    const uint32_t slot_s = smem_u32(slotp);
+    const int l = q / ws.nst, s = q - l * ws.nst;
+    const int r0 = s * ws.RS;
+    const int nrec = min(ws.RS, n - r0);
+    float2 sp = make_float2(0.f, 0.f), spp = sp, sop = sp;
+#pragma unroll 2
+    for (int r = 0; r < nrec; ++r) {
+      const uint32_t rec = slot_s + r * R;
+      float wv[2 * ((K + 1) / 2)];
+      uint32_t rv[2 * ((K + 3) / 4)];
+      if constexpr (K == 2) {
+        uint32_t u0;
+        lds_v2(rec, u0, rv[0]);
+        wv[0] = __uint_as_float(u0);
+      } else {
+#pragma unroll
+        for (int c = 0; c < ((rec_implicit(K) ? K - 1 : K) + 1) / 2; ++c)
+          lds_v2(rec + 8 * c, wv[2 * c], wv[2 * c + 1]);
+#pragma unroll
+        for (int c = 0; c < (K + 3) / 4; ++c) lds_v2(rec + RO + 8 * c, rv[2 * c], rv[2 * c + 1]);
+      }
+      const float2 o = h2f2(lds_u32(tbase + ((uint32_t)(off + r0 + r) << 7)));
+      float2 p;
+      if constexpr (rec_implicit(K)) {
+        float2 yv[K];
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+          yv[kk] = h2f2(lds_u32(tbase + (row << 7)));
+        }
+        p = yv[K - 1];
+#pragma unroll
+        for (int kk = 0; kk < K - 1; ++kk) {
+          const float2 d = make_float2(__fsub_rn(yv[kk].x, yv[K - 1].x), __fsub_rn(yv[kk].y, yv[K - 1].y));
+          p = __ffma2_rn(make_float2(wv[kk], wv[kk]), d, p);
+        }
+      } else {
+        p = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+          p = __ffma2_rn(make_float2(wv[kk], wv[kk]), h2f2(lds_u32(tbase + (row << 7))), p);
+        }
+      }
+      sp = __fadd2_rn(sp, p);
+      spp = __ffma2_rn(p, p, spp);
+      sop = __ffma2_rn(o, p, sop);
+    }
+    Sp0 += sp.x; Sp1 += sp.y;
+    Spp0 += spp.x; Spp1 += spp.y;
+    Sop0 += sop.x; Sop1 += sop.y;
+    __syncwarp();
+    if (lane == 0 && q + 2 < ws.total) issue_stage(ws, q + 2, slotp, bars + (g & 1));
+    if (s == ws.nst - 1) {
+      const double nn = (double)n;
+      const double Sp[2] = {Sp0, Sp1}, Spp[2] = {Spp0, Spp1}, Sop[2] = {Sop0, Sop1};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double m2o = Soo[h] - So[h] * So[h] / nn;
+        const double m2p = Spp[h] - Sp[h] * Sp[h] / nn;
+        const double com = Sop[h] - So[h] * Sp[h] / nn;
+        float rr = __int_as_float(0x7fc00000);
+        if (!ocst[h] && m2o > 0.0 && m2p > 0.0) rr = (float)fmin(1.0, fmax(-1.0, com / sqrt(m2o * m2p)));
+        if (tid[h] >= 0) a.rhoT[(size_t)tid[h] * a.ldr + a.lib_col[lib0 + l]] = rr;
+      }
+      Sp0 = Sp1 = Spp0 = Spp1 = Sop0 = Sop1 = 0.0;
+    }
+  }
+  qglob += ws.total;
+}
+
+template <bool RESIDENT, bool H16>
 __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(LookupArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   float* tgt = reinterpret_cast<float*>(smem);
@@ -260,11 +394,12 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
     const int blk = a.g_blk0[g] + (int)(rem - (int64_t)lsub * nblk);
     const int E = a.g_E[g];
 
-    // stage the 32-target block, time-major
+    // stage the target block (32 fp32 or 64 fp16 targets: 128 bytes per row), time-major
     if (RESIDENT) {
-      const float4* src = reinterpret_cast<const float4*>(a.Y + (size_t)blk * 32);
+      const float4* src = H16 ? reinterpret_cast<const float4*>(reinterpret_cast<const uint8_t*>(a.Y) + (size_t)blk * 128)
+                              : reinterpret_cast<const float4*>(a.Y + (size_t)blk * 32);
       float4* dst = reinterpret_cast<float4*>(tgt);
-      const int64_t ld4 = a.ldy / 4;
+      const int64_t ld4 = H16 ? a.ldy / 8 : a.ldy / 4;
       for (int v = threadIdx.x; v < a.T * 8; v += blockDim.x) {
         const int t = v >> 3, c = v & 7;
         dst[v] = src[(size_t)t * ld4 + c];
@@ -278,7 +413,13 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
     if (nl > 0) {
       const int k = E + 1;
       switch (k) {
-#define CMB_K(kk) case kk: warp_libraries<kk, RESIDENT>(a, RESIDENT ? tgt : a.Y + (size_t)blk * 32, ring, wbars, qglob, E, lib0, nl, blk * 32); break;
+#define CMB_K(kk)                                                                                   \
+  case kk:                                                                                          \
+    if constexpr (H16)                                                                              \
+      warp_libraries_h16<kk>(a, reinterpret_cast<const uint8_t*>(tgt), ring, wbars, qglob, E, lib0, nl, blk * 64); \
+    else                                                                                            \
+      warp_libraries<kk, RESIDENT>(a, RESIDENT ? tgt : a.Y + (size_t)blk * 32, ring, wbars, qglob, E, lib0, nl, blk * 32); \
+    break;
         CMB_K(2) CMB_K(3) CMB_K(4) CMB_K(5) CMB_K(6) CMB_K(7) CMB_K(8) CMB_K(9) CMB_K(10)
         CMB_K(11) CMB_K(12) CMB_K(13) CMB_K(14) CMB_K(15) CMB_K(16) CMB_K(17) CMB_K(18) CMB_K(19)
         CMB_K(20) CMB_K(21) CMB_K(22) CMB_K(23) CMB_K(24) CMB_K(25) CMB_K(26) CMB_K(27) CMB_K(28)
@@ -308,7 +449,8 @@ int lookup_stage_bytes(int T, int max_rec_bytes) {
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st) {
   const bool resident = a.stage_bytes != kNonResidentStage;
   const int smem = (resident ? a.T * 128 : 0) + kLookupWarps * 2 * a.stage_bytes + kLookupWarps * 2 * 8;
-  auto kern = resident ? lookup_xmap_kernel<true> : lookup_xmap_kernel<false>;
+  auto kern = !resident ? lookup_xmap_kernel<false, false>
+                        : (a.h16 ? lookup_xmap_kernel<true, true> : lookup_xmap_kernel<true, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   count_launch();

@@ -5,6 +5,7 @@
 #include "cmb_common.cuh"
 #include "kernels.cuh"
 
+#include <cuda_fp16.h>
 #include <float.h>
 
 namespace cmb {
@@ -96,6 +97,38 @@ __global__ void obs_moments_kernel(const float* __restrict__ Y, int64_t ldy, int
   bool c = true;
   for (int t = 0; t < n; ++t) {
     const float v = Y[(int64_t)(off + t) * ldy + s];
+    a += (double)v;
+    b += (double)v * (double)v;
+    c = c && (v == first);
+  }
+  s1[s] = a;
+  s2[s] = b;
+  cst[s] = c ? 1 : 0;
+}
+
+// fp16 target staging (opt-in lookup mode, CMB_LOOKUP_FP16=1): per slot the
+// centred series is scaled into [-1, 1] (rho is invariant to the scale), rounded
+// to fp16, and the observed-segment moments are taken from the rounded values
+// so Pearson is evaluated on one consistent set of numbers.
+__global__ void targets_to_half_kernel(const float* __restrict__ Y, int64_t ldy, int T, int tau,
+                                       const int32_t* __restrict__ slot_E, int64_t slots,
+                                       __half* __restrict__ Yh, double* __restrict__ s1,
+                                       double* __restrict__ s2, uint8_t* __restrict__ cst) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= slots) return;
+  float m = 0.f;
+  for (int t = 0; t < T; ++t) m = fmaxf(m, fabsf(Y[(int64_t)t * ldy + s]));
+  const float inv = (m > 0.f) ? 1.f / m : 1.f;
+  for (int t = 0; t < T; ++t) Yh[(int64_t)t * ldy + s] = __float2half_rn(Y[(int64_t)t * ldy + s] * inv);
+  const int E = slot_E[s];
+  if (E <= 0) { s1[s] = 0; s2[s] = 0; cst[s] = 1; return; }
+  const int off = (E - 1) * tau;
+  const int n = T - off;
+  double a = 0.0, b = 0.0;
+  const float first = __half2float(Yh[(int64_t)off * ldy + s]);
+  bool c = true;
+  for (int t = 0; t < n; ++t) {
+    const float v = __half2float(Yh[(int64_t)(off + t) * ldy + s]);
     a += (double)v;
     b += (double)v * (double)v;
     c = c && (v == first);
@@ -340,6 +373,16 @@ cudaError_t launch_obs_moments(const float* Y, int64_t ldy, int T, int tau, cons
   count_launch();
   obs_moments_kernel<<<(unsigned)((slots + 127) / 128), 128, 0, st>>>(Y, ldy, T, tau, slot_E, slots,
                                                                      s, ss, cst);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_targets_to_half(const float* Y, int64_t ldy, int T, int tau, const int32_t* slot_E,
+                                   int64_t slots, void* Yh, double* s, double* ss, uint8_t* cst,
+                                   cudaStream_t st) {
+  if (slots == 0) return cudaSuccess;
+  count_launch();
+  targets_to_half_kernel<<<(unsigned)((slots + 127) / 128), 128, 0, st>>>(
+      Y, ldy, T, tau, slot_E, slots, reinterpret_cast<__half*>(Yh), s, ss, cst);
   return cudaGetLastError();
 }
 
