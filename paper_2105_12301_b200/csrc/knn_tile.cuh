@@ -50,7 +50,6 @@ constexpr int kHalf = 32 * kRun;      // offset of the second run
 constexpr int kTile = 2 * kHalf;      // candidates per warp tile
 constexpr int kEB = 4;                // dimensions per unrolled block
 constexpr int kNW = kRun + kEB - 1;   // window pairs per block
-constexpr int kScr = kTC + 2;         // scratch row stride (floats): 8-byte aligned, conflict free
 constexpr int kScrWarp = 800;        // per-warp scratch: carried + tile pool, or E_HI x 33 lane minima
 
 // pair-packed series: pair p = (x[p], x[p + kHalf]) at index zi(p), one pad pair per 4
@@ -58,24 +57,6 @@ __device__ __forceinline__ int zi(int p) { return p + (p >> 2); }
 __host__ __device__ constexpr int z_len(int n) { return n + (n >> 2) + 1; }
 __device__ __forceinline__ float xval(const float2* Z, int p) { return Z[zi(p)].x; }
 
-// candidate of hit bit c (c < kRun: first run, else second run) and its scratch slot
-__device__ __forceinline__ int cand_of(int p, int c) { return c < kRun ? p + c : p + kHalf + (c - kRun); }
-__device__ __forceinline__ int slot_of(int c) { return c < kRun ? 2 * c : 2 * (c - kRun) + 1; }
-
-// ascending bitonic sort of one float per lane
-__device__ __forceinline__ float warp_sort32f(float v) {
-  const int lane = lane_id();
-#pragma unroll
-  for (int size = 2; size <= 32; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      const float o = __shfl_xor_sync(CMB_FULL, v, stride);
-      const bool keep_min = ((lane & stride) == 0) == ((lane & size) == 0);
-      v = keep_min ? fminf(v, o) : fmaxf(v, o);
-    }
-  }
-  return v;
-}
 
 // ascending bitonic sort of one key per lane over groups of W lanes
 template <int W>
