@@ -396,23 +396,27 @@ static __device__ __noinline__ unsigned lane_finish(const KnnArgs* __restrict__ 
     int lc = c[0];
     const int bc = c[1];
     {
+      // insertion by (distance, index): binary search for the slot, then an
+      // unrolled block move (independent loads/stores pipeline, unlike a
+      // compare-and-shift chain whose every step waits on the previous load)
       for (int b = 0; b < bc; ++b) {
         const Entry x = Be[b];
         const unsigned long long key = pack_key(x.d, x.j);
-        int pos;
+        int n = lc;
         if (lc == Kp) {
           if (key >= pack_key(Le[Kp - 1].d, Le[Kp - 1].j)) continue;
-          pos = Kp - 1;
+          n = Kp - 1;  // the last entry drops out
         } else {
-          pos = lc++;
+          ++lc;
         }
-        while (pos > 0) {
-          const Entry y = Le[pos - 1];
-          if (pack_key(y.d, y.j) < key) break;
-          Le[pos] = y;
-          --pos;
+        int lo = 0, hi = n;
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (pack_key(Le[mid].d, Le[mid].j) < key) lo = mid + 1; else hi = mid;
         }
-        Le[pos] = x;
+#pragma unroll 4
+        for (int m = n; m > lo; --m) Le[m] = Le[m - 1];
+        Le[lo] = x;
       }
     }
     c[0] = lc;

@@ -161,7 +161,10 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
     const int r0 = s * ws.RS;
     const int nrec = min(ws.RS, n - r0);
     float sp = 0.f, spp = 0.f, sop = 0.f;
-#pragma unroll 2
+    // non-resident gathers come from L2: unroll over points so enough independent
+    // loads are in flight (small k would otherwise leave the warp latency-bound)
+    constexpr int UNR = RESIDENT ? 2 : (K <= 3 ? 8 : (K <= 8 ? 4 : 2));
+#pragma unroll UNR
     for (int r = 0; r < nrec; ++r) {
       const uint32_t rec = slot_s + r * R;
       // broadcast reads as 8-byte loads (one shared wavefront each; a
