@@ -110,3 +110,21 @@ def test_convergence_sampling_matches_oracle_rule():
     assert all(np.array_equal(x, y) for x, y in zip(a, b))
     with pytest.raises(P.ParameterError):
         sample_libraries(50, [60], 1, seed=0)
+
+
+def test_bench_roofline_models():
+    """bench.py's algorithmic byte and shared-memory wavefront models (K3)
+    on a hand-countable workload: 2 libraries, targets E* = [1, 1, 2], T = 10."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    estar = np.array([1, 1, 2], dtype=np.int32)
+    T, libs = 10, 2
+    # E=1: N_E=2, n_E=10, k=2; E=2: N_E=1, n_E=9, k=3  (B_pair = 4 n + 8 n k / N_E + 4)
+    want = libs * (2 * (4 * 10 + 4) + 8 * 10 * 2) + libs * (1 * (4 * 9 + 4) + 8 * 9 * 3)
+    assert bench.lookup_alg_bytes(estar, libs, T) == want
+    # one 32-target block per E group; per point k gathers + record loads + 1 observed load
+    # (k=2: 1 record load; k=3: 1 weight + 1 row load)
+    assert bench.lookup_alg_wavefronts(estar, libs, T) == libs * (10 * (2 + 1 + 1) + 9 * (3 + 2 + 1))
