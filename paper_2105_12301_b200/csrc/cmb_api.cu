@@ -463,7 +463,9 @@ int cmb_shutdown(void) {
     cudaSetDevice(c->dev);
     for (auto& b : c->buf) b.release();
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     c->stream = nullptr;
+    c->copy_stream = nullptr;
     c->ready = false;
   }
   g_ctx.clear();
