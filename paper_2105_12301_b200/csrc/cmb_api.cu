@@ -780,49 +780,126 @@ int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E,
     CMB_PARAM(lib_ids[p] >= 0 && lib_ids[p] < N && tgt_ids[p] >= 0 && tgt_ids[p] < N, "bad pair %lld",
               (long long)p);
   if (P == 0 || n_sizes == 0) return CMB_OK;
+  CMB_PARAM(len <= 65535, "series length %lld exceeds the 16-bit table format", (long long)len);
   CMB_CTX(dev);
+  // distinct libraries and targets of the pair list
+  std::vector<int32_t> libs, tgts;
+  std::vector<int> lib_ix(N, -1), tgt_ix(N, -1);
+  for (int64_t p = 0; p < P; ++p) {
+    if (lib_ix[lib_ids[p]] < 0) { lib_ix[lib_ids[p]] = (int)libs.size(); libs.push_back(lib_ids[p]); }
+    if (tgt_ix[tgt_ids[p]] < 0) { tgt_ix[tgt_ids[p]] = (int)tgts.size(); tgts.push_back(tgt_ids[p]); }
+  }
+  const int64_t NL = (int64_t)libs.size(), NT = (int64_t)tgts.size();
+  const int64_t PL = NL * n_sizes * samples;  // pseudo-libraries (library, size, sample)
+  // targets: one E group padded to 32-slot blocks, slot -> target row of the output chunk
+  const int64_t slots = (NT + 31) / 32 * 32;
+  std::vector<int32_t> slot_series(slots, -1), slot_row(slots, -1), slot_E(slots, 0);
+  for (int64_t t = 0; t < NT; ++t) { slot_series[t] = tgts[t]; slot_row[t] = (int32_t)t; slot_E[t] = E; }
+  // device staging: X (fp64 for the exact tables, fp32 for the targets), samples, targets
   CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * len));
+  CMB_CUDA(ctx->buf[B_X32].ensure(sizeof(float) * N * len + 256));
+  CMB_CUDA(ctx->buf[B_ERR].ensure(sizeof(float) * N));
   CMB_CUDA(ctx->buf[B_A].ensure(sizeof(int32_t) * total_pts + 16));
+  CMB_CUDA(ctx->buf[B_B].ensure(sizeof(int64_t) * (n_sizes + 1) + sizeof(int32_t) * n_sizes + 16));
+  CMB_CUDA(ctx->buf[B_LIBROWS].ensure(sizeof(int32_t) * NL));
+  CMB_CUDA(ctx->buf[B_SLOT_TGT].ensure(4 * slots));
+  CMB_CUDA(ctx->buf[B_SLOT_E].ensure(4 * slots));
+  CMB_CUDA(ctx->buf[B_OBS_S].ensure(8 * slots));
+  CMB_CUDA(ctx->buf[B_OBS_SS].ensure(8 * slots));
+  CMB_CUDA(ctx->buf[B_OBS_C].ensure(slots));
+  CMB_CUDA(ctx->buf[B_Y].ensure(sizeof(float) * len * slots));
+  CMB_CUDA(ctx->buf[B_MEAN].ensure(8 * N));
+  CMB_CUDA(ctx->buf[B_COUNTER].ensure(16));
   CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X64].p, X, sizeof(double) * N * len, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(launch_demote(ctx->buf[B_X64].as<double>(), N, len, ctx->buf[B_X32].as<float>(),
+                         ctx->buf[B_ERR].as<float>(), st));
   CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_A].p, pts, sizeof(int32_t) * total_pts, cudaMemcpyHostToDevice, st));
-  const double* x64 = ctx->buf[B_X64].as<double>();
-  // pairs grouped by library
-  std::vector<std::vector<std::pair<int64_t, int>>> by_lib(N);
-  for (int64_t p = 0; p < P; ++p) by_lib[lib_ids[p]].push_back({p, tgt_ids[p]});
-  std::vector<double> host_rho;
-  for (int64_t lib = 0; lib < N; ++lib) {
-    const auto& pr = by_lib[lib];
-    if (pr.empty()) continue;
-    const int64_t M = (int64_t)pr.size();
-    CMB_CUDA(ctx->buf[B_C].ensure(sizeof(double) * M * len));
-    CMB_CUDA(ctx->buf[B_D].ensure(sizeof(double) * M * n));
-    CMB_CUDA(ctx->buf[B_E].ensure(sizeof(double) * M * n_sizes * samples));
-    for (int64_t m = 0; m < M; ++m)
-      CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_C].as<double>() + m * len, x64 + (int64_t)pr[m].second * len,
-                               sizeof(double) * len, cudaMemcpyDeviceToDevice, st));
-    for (int s = 0; s < n_sizes; ++s) {
-      CMB_CUDA(ctx->buf[B_B].ensure(sizeof(int64_t) * samples * n * k));
-      CMB_CUDA(ctx->buf[B_LIBCOL].ensure(sizeof(double) * samples * n * k));
-      CMB_CUDA(launch_restricted_tables(x64 + lib * len, (int)n, E, tau, k,
-                                        ctx->buf[B_A].as<int32_t>() + size_off[s], sizes[s], samples,
-                                        ctx->buf[B_B].as<int64_t>(), ctx->buf[B_LIBCOL].as<double>(), st));
-      for (int q = 0; q < samples; ++q) {
-        const size_t toff = (size_t)q * n * k;
-        CMB_CUDA(launch_lookup64(ctx->buf[B_B].as<int64_t>() + toff, ctx->buf[B_LIBCOL].as<double>() + toff,
-                                 n, k, (E - 1) * tau, ctx->buf[B_C].as<double>(), len, M,
-                                 ctx->buf[B_D].as<double>(),
-                                 ctx->buf[B_E].as<double>() + ((size_t)s * samples + q) * M, st));
-      }
-    }
-    host_rho.resize((size_t)M * n_sizes * samples);
-    CMB_CUDA(cudaMemcpyAsync(host_rho.data(), ctx->buf[B_E].p, sizeof(double) * host_rho.size(),
-                             cudaMemcpyDeviceToHost, st));
+  int64_t* d_size_off = ctx->buf[B_B].as<int64_t>();
+  int32_t* d_sizes = reinterpret_cast<int32_t*>(d_size_off + n_sizes + 1);
+  CMB_CUDA(cudaMemcpyAsync(d_size_off, size_off.data(), sizeof(int64_t) * (n_sizes + 1), cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(d_sizes, sizes, sizeof(int32_t) * n_sizes, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_LIBROWS].p, libs.data(), sizeof(int32_t) * NL, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_SLOT_TGT].p, slot_series.data(), 4 * slots, cudaMemcpyHostToDevice, st));
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_SLOT_E].p, slot_E.data(), 4 * slots, cudaMemcpyHostToDevice, st));
+  const float* x32 = ctx->buf[B_X32].as<float>();
+  CMB_CUDA(launch_series_stats(x32, N, len, len, ctx->buf[B_MEAN].as<double>(), st));
+  CMB_CUDA(launch_build_targets(x32, len, ctx->buf[B_MEAN].as<double>(), ctx->buf[B_SLOT_TGT].as<int32_t>(),
+                                slots, (int)len, ctx->buf[B_Y].as<float>(), slots, st));
+  CMB_CUDA(launch_obs_moments(ctx->buf[B_Y].as<float>(), slots, (int)len, tau, ctx->buf[B_SLOT_E].as<int32_t>(),
+                              slots, ctx->buf[B_OBS_S].as<double>(), ctx->buf[B_OBS_SS].as<double>(),
+                              ctx->buf[B_OBS_C].as<uint8_t>(), st));
+  // the lookup writes rho_T[row][column]: slot rows are output rows
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_SLOT_TGT].p, slot_row.data(), 4 * slots, cudaMemcpyHostToDevice, st));
+  // chunks of pseudo-libraries: tables (<= ~4 GB) and their rho_T columns
+  const size_t stride = rec_lib_stride(k, n);
+  const int LS = 64;
+  int64_t C = std::max<int64_t>(LS, (int64_t)(((size_t)4 << 30) / stride) / LS * LS);
+  C = std::min<int64_t>(C, (PL + LS - 1) / LS * LS);
+  const int64_t ldr = (C + 3) / 4 * 4;
+  CMB_CUDA(ctx->buf[B_TAB].ensure(stride * C + 256));
+  CMB_CUDA(ctx->buf[B_RHOT].ensure(sizeof(float) * slots * ldr));
+  CMB_CUDA(ctx->buf[B_LIBCOL].ensure(sizeof(int64_t) * C));
+  std::vector<int64_t> cols(C);
+  for (int64_t c = 0; c < C; ++c) cols[c] = c;
+  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_LIBCOL].p, cols.data(), sizeof(int64_t) * C, cudaMemcpyHostToDevice, st));
+  const int stage = lookup_stage_bytes((int)len, rec_bytes(k));
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->dev);
+  // requested pairs by library index, for the scatter
+  std::vector<std::vector<std::pair<int64_t, int>>> by_lib(NL);
+  for (int64_t p = 0; p < P; ++p) by_lib[lib_ix[lib_ids[p]]].push_back({p, tgt_ix[tgt_ids[p]]});
+  std::vector<float> chunk_rho;
+  for (int64_t c0 = 0; c0 < PL; c0 += C) {
+    const int64_t nc = std::min<int64_t>(C, PL - c0);
+    CMB_CUDA(launch_fill_nan(ctx->buf[B_RHOT].as<float>(), slots, nc, ldr, st));
+    CMB_CUDA(launch_restricted_records(ctx->buf[B_X64].as<double>(), len, ctx->buf[B_LIBROWS].as<int32_t>(),
+                                       (int)n, E, tau, ctx->buf[B_A].as<int32_t>(), d_size_off, d_sizes,
+                                       n_sizes, samples, c0, nc, ctx->buf[B_TAB].as<uint8_t>(), st));
+    LookupArgs la;
+    memset(&la, 0, sizeof(la));
+    la.Y = ctx->buf[B_Y].as<float>();
+    la.ldy = slots;
+    la.T = (int)len;
+    la.tau = tau;
+    la.ngroups = 1;
+    la.g_E[0] = E;
+    la.g_blk0[0] = 0;
+    la.g_nblk[0] = (int)(slots / 32);
+    la.slot_tgt = ctx->buf[B_SLOT_TGT].as<int32_t>();
+    la.obs_s = ctx->buf[B_OBS_S].as<double>();
+    la.obs_ss = ctx->buf[B_OBS_SS].as<double>();
+    la.obs_const = ctx->buf[B_OBS_C].as<uint8_t>();
+    la.tab[E] = ctx->buf[B_TAB].as<uint8_t>();
+    la.nlib = (int)nc;
+    la.lib_col = ctx->buf[B_LIBCOL].as<int64_t>();
+    la.LS = LS;
+    la.n_lsub = (int)((nc + LS - 1) / LS);
+    la.g_item0[0] = 0;
+    la.n_items = (int64_t)la.n_lsub * la.g_nblk[0];
+    la.g_item0[1] = la.n_items;
+    la.counter = ctx->buf[B_COUNTER].as<int>();
+    la.rhoT = ctx->buf[B_RHOT].as<float>();
+    la.ldr = ldr;
+    la.stage_bytes = stage;
+    CMB_CUDA(cudaMemsetAsync(la.counter, 0, sizeof(int), st));
+    CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(la.n_items, dev_sms), st));
+    chunk_rho.resize((size_t)NT * ldr);
+    CMB_CUDA(cudaMemcpy2DAsync(chunk_rho.data(), sizeof(float) * ldr, ctx->buf[B_RHOT].p, sizeof(float) * ldr,
+                               sizeof(float) * nc, NT, cudaMemcpyDeviceToHost, st));
     CMB_CUDA(cudaStreamSynchronize(st));
-    for (int64_t m = 0; m < M; ++m)
-      for (int s = 0; s < n_sizes; ++s)
-        for (int q = 0; q < samples; ++q)
-          rho_out[((size_t)pr[m].first * n_sizes + s) * samples + q] =
-              host_rho[((size_t)s * samples + q) * M + m];
+    // scatter: pseudo-library pl = (li * n_sizes + s) * samples + q
+    const int64_t ls0 = c0 / samples, ls1 = (c0 + nc + samples - 1) / samples;
+    for (int64_t ls = ls0; ls < ls1; ++ls) {
+      const int64_t li = ls / n_sizes;
+      const int s = (int)(ls % n_sizes);
+      for (const auto& pr : by_lib[li])
+        for (int q = 0; q < samples; ++q) {
+          const int64_t pl = ls * samples + q;
+          if (pl < c0 || pl >= c0 + nc) continue;
+          const float v = chunk_rho[(size_t)pr.second * ldr + (pl - c0)];
+          rho_out[((size_t)pr.first * n_sizes + s) * samples + q] = (double)v;
+        }
+    }
   }
   return CMB_OK;
 }

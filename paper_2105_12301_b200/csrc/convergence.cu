@@ -10,9 +10,11 @@
 // predicted at all points (Tp = 0) and scored with Pearson.
 //
 // The restricted tables are built exactly in float64 (reference operation
-// order, no fused multiply-add) -- the candidate sets are small -- by one warp
-// per query row with a register list; the lookup reuses the float64 kernels of
-// the public lookup_batch path.
+// order, no fused multiply-add) by one warp per query row with a register
+// list.  Every (library, size, sample) is a "pseudo-library": its table is
+// written in the cross-map record format (cmb_common.cuh rec_*), and the
+// shared-memory-resident lookup of the cross map (lookup.cu) scores all targets
+// of the E group against a chunk of pseudo-libraries per launch.
 #include "cmb_common.cuh"
 #include "kernels.cuh"
 
@@ -24,15 +26,27 @@ namespace {
 
 __device__ __forceinline__ double inf64() { return __longlong_as_double(0x7ff0000000000000ll); }
 
-// grid: (ceil(n / 8), samples); block 256 = 8 warps, one row each
-__global__ void restricted_table_kernel(const double* __restrict__ x, int n, int E, int tau, int k,
-                                        const int32_t* __restrict__ pts, int npts,
-                                        int64_t* __restrict__ idx_out, double* __restrict__ w_out) {
+// Same selection, one warp per (pseudo-library, row), writing xmap records
+// (fp32 weights from the exact fp64 ones, u16 rows idx + (E-1) tau).
+// grid: (n_pseudo, ceil(n / 8)); pseudo-library pl = chunk0 + blockIdx.x is
+// (library index li, size s, sample q) = ((pl / samples) / n_sizes, ...).
+__global__ void restricted_records_kernel(const double* __restrict__ X, int64_t len,
+                                          const int32_t* __restrict__ libs, int n, int E, int tau,
+                                          int k, const int32_t* __restrict__ pts,
+                                          const int64_t* __restrict__ size_off,
+                                          const int32_t* __restrict__ sizes, int n_sizes, int samples,
+                                          int64_t chunk0, uint8_t* __restrict__ tab) {
   const int lane = lane_id();
-  const int row = blockIdx.x * 8 + warp_id();
-  const int smp = blockIdx.y;
+  const int row = blockIdx.y * 8 + warp_id();
+  const int64_t pl = chunk0 + blockIdx.x;
   if (row >= n) return;
-  const int32_t* S = pts + (size_t)smp * npts;
+  const int q = (int)(pl % samples);
+  const int64_t ls = pl / samples;
+  const int s = (int)(ls % n_sizes);
+  const int li = (int)(ls / n_sizes);
+  const double* x = X + (int64_t)libs[li] * len;
+  const int npts = sizes[s];
+  const int32_t* S = pts + size_off[s] + (int64_t)q * npts;
   double dd = inf64();
   int jj = 0x7fffffff;
   double thr = inf64();
@@ -68,7 +82,6 @@ __global__ void restricted_table_kernel(const double* __restrict__ x, int n, int
       m &= __ballot_sync(CMB_FULL, D < thr);
     }
   }
-  // simplex weights on the exact distances (knn.py:194-202)
   const double dist = (lane < k) ? sqrt(dd) : 0.0;
   double scale = __shfl_sync(CMB_FULL, dist, 0);
   if (scale == 0.0) {
@@ -78,21 +91,23 @@ __global__ void restricted_table_kernel(const double* __restrict__ x, int n, int
   double raw = 0.0;
   if (lane < k) raw = fmax(exp(-dist / scale), DBL_MIN);
   const double wgt = raw / warp_sum_d(raw);
-  if (lane < k) {
-    const size_t at = ((size_t)smp * n + row) * k + lane;
-    idx_out[at] = jj;
-    w_out[at] = wgt;
-  }
+  uint8_t* rec = tab + (size_t)blockIdx.x * rec_lib_stride(k, n) + (size_t)row * rec_bytes(k);
+  if (lane < rec_nw(k)) reinterpret_cast<float*>(rec)[lane] = (lane < k) ? (float)wgt : 0.f;
+  if (lane < rec_nr(k))
+    reinterpret_cast<uint16_t*>(rec + rec_row_off(k))[lane] = (lane < k) ? (uint16_t)(jj + (E - 1) * tau) : (uint16_t)0;
 }
 
 }  // namespace
 
-cudaError_t launch_restricted_tables(const double* x, int n, int E, int tau, int k, const int32_t* pts,
-                                     int npts, int samples, int64_t* idx, double* w, cudaStream_t st) {
-  if (n <= 0 || samples <= 0) return cudaSuccess;
-  dim3 grid((n + 7) / 8, samples);
+cudaError_t launch_restricted_records(const double* X, int64_t len, const int32_t* libs, int n, int E,
+                                      int tau, const int32_t* pts, const int64_t* size_off,
+                                      const int32_t* sizes, int n_sizes, int samples, int64_t chunk0,
+                                      int64_t n_pseudo, uint8_t* tab, cudaStream_t st) {
+  if (n <= 0 || n_pseudo <= 0) return cudaSuccess;
+  dim3 grid((unsigned)n_pseudo, (n + 7) / 8);
   count_launch();
-  restricted_table_kernel<<<grid, 256, 0, st>>>(x, n, E, tau, k, pts, npts, idx, w);
+  restricted_records_kernel<<<grid, 256, 0, st>>>(X, len, libs, n, E, tau, E + 1, pts, size_off, sizes,
+                                                  n_sizes, samples, chunk0, tab);
   return cudaGetLastError();
 }
 

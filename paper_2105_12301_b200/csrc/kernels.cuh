@@ -108,8 +108,11 @@ cudaError_t launch_pearson(const double* a, const double* b, int64_t n, double* 
 cudaError_t launch_lookup64(const int64_t* idx, const double* w, int64_t n, int k, int offset,
                             const double* Y, int64_t len, int64_t M, double* pred,
                             double* rho, cudaStream_t st);
-cudaError_t launch_restricted_tables(const double* x, int n, int E, int tau, int k, const int32_t* pts,
-                                     int npts, int samples, int64_t* idx, double* w, cudaStream_t st);
+cudaError_t launch_restricted_records(const double* X, int64_t len, const int32_t* libs, int n, int E,
+                                      int tau, const int32_t* pts, const int64_t* size_off,
+                                      const int32_t* sizes, int n_sizes, int samples, int64_t chunk0,
+                                      int64_t n_pseudo, uint8_t* tab, cudaStream_t st);
+
 cudaError_t launch_transpose_f32(const float* src, int64_t rows, int64_t cols, int64_t lds,
                                  float* dst, int64_t ldd, cudaStream_t st);
 
