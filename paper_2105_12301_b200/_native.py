@@ -19,7 +19,8 @@ import numpy as np
 from .errors import (CrossmapError, DeviceError, ParameterError, SeriesTooShortError,
                      ZeroVarianceError)
 
-LIB_PATH = Path(__file__).resolve().parent / "libcmb200.so"
+# CMB_LIB names an alternative build of the same library (A/B timing of two builds).
+LIB_PATH = Path(os.environ.get("CMB_LIB") or Path(__file__).resolve().parent / "libcmb200.so")
 LIB_VERSION = 100  # 0.1.0
 
 _i32, _i64, _dbl, _vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p

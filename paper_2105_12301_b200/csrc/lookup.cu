@@ -113,6 +113,29 @@ __device__ __forceinline__ void issue_stage(const WarpStream& ws, int q, uint8_t
   bulk_g2s(slot, src, bytes, bar);
 }
 
+// Prediction of one embedded point from its record in a shared-memory stage
+// (used once per library for the accumulation shift below).  y(row) reads the
+// lane's target sample; the arithmetic matches the main loop.
+template <int K, typename Y>
+__device__ __forceinline__ float record_predict(uint32_t rec, Y y) {
+  constexpr int RO = rec_row_off(K);
+  const auto row = [&](int kk) {
+    return __byte_perm(lds_u32(rec + RO + 4 * (kk >> 1)), 0, (kk & 1) ? 0x4432 : 0x4410);
+  };
+  if constexpr (rec_implicit(K)) {
+    const float ylast = y(row(K - 1));
+    float p = ylast;
+#pragma unroll
+    for (int kk = 0; kk < K - 1; ++kk) p = __fmaf_rn(lds_f32(rec + 4 * kk), __fsub_rn(y(row(kk)), ylast), p);
+    return p;
+  } else {
+    float p = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) p = __fmaf_rn(lds_f32(rec + 4 * kk), y(row(kk)), p);
+    return p;
+  }
+}
+
 // RESIDENT: targets staged in shared memory with row stride 32; otherwise
 // gathered from the time-major global array (row stride ldy) through L1/L2.
 template <int K, bool RESIDENT>
@@ -151,13 +174,24 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
   }
   __syncwarp();
 
+  // Moments are accumulated about a per-(library, target) shift, the prediction
+  // of the library's first point: m2p and the comoment are shift-invariant, and
+  // a near-constant prediction (e.g. from a constant library) would otherwise
+  // cancel catastrophically in sum p^2 - (sum p)^2 / n.
   double Sp = 0.0, Spp = 0.0, Sop = 0.0;
+  float shift = 0.f;
   for (int q = 0; q < ws.total; ++q) {
     const uint32_t g = qglob + q;
     uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
+    const int l = q / ws.nst, s = q - l * ws.nst;
     mbar_wait(bars + (g & 1), (g >> 1) & 1);
     const uint32_t slot_s = smem_u32(slotp);
-    const int l = q / ws.nst, s = q - l * ws.nst;
+    if (s == 0) {
+      if (RESIDENT)
+        shift = record_predict<K>(slot_s, [&](uint32_t row) { return lds_f32(tbase + (row << 7)); });
+      else
+        shift = record_predict<K>(slot_s, [&](uint32_t row) { return tcol[(int64_t)row * stride]; });
+    }
     const int r0 = s * ws.RS;
     const int nrec = min(ws.RS, n - r0);
     float sp = 0.f, spp = 0.f, sop = 0.f;
@@ -171,7 +205,7 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
       // broadcast 16-byte load costs two, so keep the compiler from merging)
       float wv[2 * ((K + 1) / 2)];
       uint32_t rv[2 * ((K + 3) / 4)];
-      float o, p = 0.f;
+      float o, p = -shift;
       if constexpr (K == 2) {
         // [w0][r0 r1]: the last weight is 1 - w0, p = y1 + w0 (y0 - y1)
         uint32_t u0;
@@ -204,7 +238,7 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
             yv[kk] = tcol[(int64_t)row * stride];
           }
         }
-        p = yv[K - 1];
+        p = __fsub_rn(yv[K - 1], shift);
 #pragma unroll
         for (int kk = 0; kk < K - 1; ++kk) p = __fmaf_rn(wv[kk], __fsub_rn(yv[kk], yv[K - 1]), p);
       } else if (RESIDENT) {

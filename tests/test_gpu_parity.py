@@ -337,3 +337,42 @@ def test_fp16_target_mode_functional(monkeypatch):
     h16 = P.xmap(X.T, est, dtype=np.float32)
     assert np.array_equal(np.isnan(h16), np.isnan(ref32))
     assert np.nanmax(np.abs(h16 - ref32)) <= 2e-3
+
+
+def test_xmap_degenerate_inputs():
+    """Edge shapes of the cross map: one series, every E* undefined, the minimum
+    series length for the largest E, constant series (undefined rows/columns)."""
+    rng = np.random.default_rng(12)
+    one = rng.random((1, 50))
+    r1 = P.xmap(one.T, [2])
+    ref1, _ = O.xmap([one[0]], [2], 1, workers=1)
+    assert r1.shape == (1, 1) and np.allclose(r1, ref1, atol=RHO_TOL, equal_nan=True)
+    X = rng.random((3, 40))
+    assert np.all(np.isnan(P.xmap(X.T, [0, 0, 0])))
+    E = 6
+    Xm = rng.random((3, (E - 1) + E + 2))                  # n_E = E + 2 exactly
+    rm = P.xmap(Xm.T, [E, E, E])
+    refm, _ = O.xmap([Xm[i] for i in range(3)], [E] * 3, 1, workers=1)
+    assert np.allclose(rm, refm, atol=RHO_TOL, equal_nan=True)
+    Xc = rng.random((4, 120))
+    Xc[2] = 0.25
+    rc = P.xmap(Xc.T, [2, 2, 2, 2])
+    refc, _ = O.xmap([Xc[i] for i in range(4)], [2] * 4, 1, workers=1)
+    assert np.array_equal(np.isnan(rc), np.isnan(refc)) and np.all(np.isnan(rc[:, 2]))
+    assert np.nanmax(np.abs(rc - refc)) <= RHO_TOL
+
+
+@pytest.mark.gpu
+def test_xmap_offset_targets():
+    """Series with a large offset and a small spread (1000 + 1e-3 noise): the
+    lookup's fp32 moments are accumulated about a per-library shift, so rho does
+    not lose its digits to the offset.  (Samples are float32 on the device, so
+    the oracle sees the same float32-rounded values.)"""
+    rng = np.random.default_rng(21)
+    X = 1000.0 + 1e-2 * np.cumsum(rng.standard_normal((5, 300)), axis=1)
+    X[1] = 1e4 + 1e-1 * np.sin(np.arange(300) * 0.3) + 1e-2 * rng.standard_normal(300)
+    X = X.astype(np.float32).astype(np.float64)
+    ests = [2, 3, 4, 1, 5]
+    r = P.xmap(X.T, ests)
+    ref, _ = O.xmap([X[i] for i in range(5)], ests, 1, workers=1)
+    assert np.nanmax(np.abs(r - ref)) <= RHO_TOL
