@@ -232,7 +232,7 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
   constexpr int EHR = (E_HI + kEB - 1) / kEB * kEB;  // dimensions rounded up to whole blocks
   __shared__ float thr_s[kWarps][E_HI];
   __shared__ float2 nq_s[kWarps][EHR];
-  __shared__ float2 ntp_s[kWarps][E_HI];
+  __shared__ float2 ntp_s[kWarps][EHR];
   __shared__ int cnt_s[kWarps][E_HI][2];
   __shared__ double s_mean;
   __shared__ int s_last;
@@ -324,8 +324,9 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
     if (lane < EHR) {
       const float q = (lane < eh) ? xval(Z, i + lane) : 0.f;
       nq_s[w][lane] = make_float2(-q, -q);
+      ntp_s[w][lane] = make_float2(kInfF, kInfF);  // inactive dimensions never hit
     }
-    for (int e = 0; e < eh; ++e) mins[e * kMinStride + lane] = kInfF;
+    for (int e = 0; e < kEB * nb; ++e) mins[e * kMinStride + lane] = kInfF;
     __syncwarp();
 
     // ---- pass 1: per-lane minima
@@ -342,18 +343,18 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
       for (int eb = 0; eb < nb; ++eb) {
         float2 W[kNW];
         block_window(Z, zb, eb, W);
+        // whole blocks without per-dimension guards: dimensions past eh or
+        // outside act compute harmlessly (their minima are never read)
 #pragma unroll
         for (int r = 0; r < kEB; ++r) {
           const int e = kEB * eb + r;
-          if (e < eh) {
-            const float2 nq = nq_s[w][e];
+          const float2 nq = nq_s[w][e];
 #pragma unroll
-            for (int c = 0; c < kRun; ++c) {
-              const float2 df = __fadd2_rn(W[c + r], nq);
-              D[c] = __ffma2_rn(df, df, D[c]);
-            }
-            if ((act >> e) & 1u) mins[e * kMinStride + lane] = fminf(mins[e * kMinStride + lane], tile_min(D));
+          for (int c = 0; c < kRun; ++c) {
+            const float2 df = __fadd2_rn(W[c + r], nq);
+            D[c] = __ffma2_rn(df, df, D[c]);
           }
+          mins[e * kMinStride + lane] = fminf(mins[e * kMinStride + lane], tile_min(D));
         }
       }
     }
@@ -380,25 +381,23 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
       for (int eb = 0; eb < nb; ++eb) {
         float2 W[kNW];
         block_window(Z, zb, eb, W);
+        // whole blocks, two dimensions per min step (FMNMX3); inactive
+        // dimensions carry ntp = +inf and never mark
 #pragma unroll
-        for (int r = 0; r < kEB; ++r) {
+        for (int r = 0; r < kEB; r += 2) {
           const int e = kEB * eb + r;
-          if (e < eh) {
-            const float2 nq = nq_s[w][e];
+          const float2 nq0 = nq_s[w][e], nq1 = nq_s[w][e + 1];
+          const float2 nt0 = ntp_s[w][e], nt1 = ntp_s[w][e + 1];
 #pragma unroll
-            for (int c = 0; c < kRun; ++c) {
-              const float2 df = __fadd2_rn(W[c + r], nq);
-              D[c] = __ffma2_rn(df, df, D[c]);
-            }
-            if ((act >> e) & 1u) {
-              const float2 nt = ntp_s[w][e];
-#pragma unroll
-              for (int c = 0; c < kRun; ++c) {
-                const float2 u = __fadd2_rn(D[c], nt);
-                Mn[c].x = fminf(Mn[c].x, u.x);
-                Mn[c].y = fminf(Mn[c].y, u.y);
-              }
-            }
+          for (int c = 0; c < kRun; ++c) {
+            const float2 df0 = __fadd2_rn(W[c + r], nq0);
+            D[c] = __ffma2_rn(df0, df0, D[c]);
+            const float2 u0 = __fadd2_rn(D[c], nt0);
+            const float2 df1 = __fadd2_rn(W[c + r + 1], nq1);
+            D[c] = __ffma2_rn(df1, df1, D[c]);
+            const float2 u1 = __fadd2_rn(D[c], nt1);
+            Mn[c].x = fminf(Mn[c].x, fminf(u0.x, u1.x));
+            Mn[c].y = fminf(Mn[c].y, fminf(u0.y, u1.y));
           }
         }
       }
