@@ -27,7 +27,7 @@
 //           over its candidates; the threshold t_E = the Kp-th smallest of the
 //           32 lane minima (Kp = k + 1 list entries) is an upper bound on the
 //           Kp-th smallest distance (Kp distinct lanes each hold a candidate
-//           <= t_E), tightened by the bound seeded from row i-1.
+//           <= t_E).  Rows are independent (no state carries from row i-1).
 //   pass 2  distances again; per (tile, E) a lane-min test against t_E, and
 //           when some lane has a candidate <= t_E the hitting lanes park their
 //           distances in a scratch row and an out-of-line collector appends
@@ -306,8 +306,7 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
   double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, acc4 = 0;
   const double shift = (a.mode == KNN_EDIM) ? s_mean : 0.0;
 
-  for (int i = max(0, r0 - 1); i < r1; ++i) {
-    const bool emit = i >= r0;
+  for (int i = r0; i < r1; ++i) {
     uint32_t act = 0;
     for (int e = 0; e < e_hi; ++e)
       if (((a.need >> e) & 1u) && i < L - e) act |= 1u << e;
@@ -457,7 +456,7 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
     __syncwarp();
 
     // ---- certification, weights, records / predictions (v4 epilogue)
-    unsigned need = lane_finish<E_HI>(&a, wl, wb, wc, lib, i, act, M, emit, true);
+    unsigned need = lane_finish<E_HI>(&a, wl, wb, wc, lib, i, act, M, true, true);
     __syncwarp();
 #pragma unroll 1
     while (need) {
