@@ -162,8 +162,7 @@ static __device__ __noinline__ int pool_round(const int* pool, int n, const floa
     const float xv = valid ? Z[zi(j + e)].x : 0.f;
     const float df = __fadd_rn(xv, nq[e].x);
     d = __fmaf_rn(df, df, d);
-    if (!((act >> e) & 1u)) continue;
-    unsigned m = __ballot_sync(CMB_FULL, d <= thr[e]);
+    unsigned m = __ballot_sync(CMB_FULL, d <= thr[e]);  // inactive dimensions: thr = -1
     if (!m) continue;
     int b0 = __shfl_sync(CMB_FULL, bc, e);
     Entry* Be = wb + tile_buf_off(mode, e);
@@ -318,7 +317,7 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
     if (lane < E_HI) {
       wc[2 * lane] = 0;
       wc[2 * lane + 1] = 0;
-      thr_s[w][lane] = kInfF;
+      thr_s[w][lane] = ((act >> lane) & 1u) ? kInfF : -1.f;  // inactive: no candidate qualifies
     }
     if (lane < EHR) {
       const float q = (lane < eh) ? xval(Z, i + lane) : 0.f;
