@@ -367,6 +367,46 @@ def run_ours(args):
                "ms_per_step": el * 1e3}
         del outp, xp
 
+    # ---- e2e at N > 1: X from pinned host memory on rank 0 (H2D), NCCL broadcast,
+    #      sharded cross map, every rank's rho slab copied to its pinned host buffer
+    #      (one PCIe link per GPU); wall time per step, max over ranks
+    if not args.no_e2e and world > 1:
+        xp = torch.from_numpy(X_host).pin_memory() if rank == 0 else None
+        Xe = torch.empty((N, T), dtype=torch.float32, device=dev)
+        host = {}
+
+        def e2e_step():
+            if rank == 0:
+                Xe.copy_(xp, non_blocking=True)
+            slab = xmap_sharded(Xe, estar, 1, broadcast=True, gather=False)
+            if "slab" not in host:
+                host["slab"] = torch.empty(slab.shape, dtype=slab.dtype).pin_memory()
+            host["slab"].copy_(slab, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            return float(host["slab"][0, 0])
+
+        for _ in range(max(1, args.warmup - 2)):
+            e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        el = (time.perf_counter() - t0) / args.steps
+        dist.barrier()
+        el_t = torch.tensor([el], dtype=torch.float64)
+        if backend == "gloo":
+            dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
+        else:
+            el_d = el_t.to(dev)
+            dist.all_reduce(el_d, op=dist.ReduceOp.MAX)
+            el_t = el_d.cpu()
+        el = float(el_t.item())
+        d2h = int(host["slab"].numel() * 4) * world
+        e2e = {"value": pairs / el, "unit": UNIT, "h2d_bytes_per_step": int(N * T * 4),
+               "d2h_bytes_per_step": d2h, "layout": "per-rank target-major slabs (library shards)",
+               "ms_per_step": el * 1e3}
+        del host, Xe, xp
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         v, sample, el = cpu_sample(X_host, estar, args.cpu_seconds, os.cpu_count() or 1)

@@ -83,7 +83,7 @@ def all_gather_rows(part, n_total: int, group=None):
 
 
 def xmap_sharded(X, estar: np.ndarray, tau: int = 1, group=None, compute: Callable | None = None,
-                 stats: np.ndarray | None = None, broadcast: bool = True):
+                 stats: np.ndarray | None = None, broadcast: bool = True, gather: bool = True):
     """Sharded all-to-all cross map.
 
     ``X``: torch tensor [N][T] float32 on this rank's device (meaningful on
@@ -91,7 +91,9 @@ def xmap_sharded(X, estar: np.ndarray, tau: int = 1, group=None, compute: Callab
     rho_T[N][G * slab] (target-major; column c of rank g's slab is library
     shard_bounds(N, G, g)[0] + c; padding columns are NaN), None elsewhere.
     ``compute`` replaces the device kernel (tests run the same plumbing on
-    CPU with gloo and an oracle-backed compute).
+    CPU with gloo and an oracle-backed compute).  ``gather=False`` skips the
+    gather and returns every rank its own slab (callers that copy each rank's
+    slab to host memory directly).
     """
     import torch
     import torch.distributed as dist
@@ -110,7 +112,7 @@ def xmap_sharded(X, estar: np.ndarray, tau: int = 1, group=None, compute: Callab
         native_shard(X, estar, tau, lo, hi, slab, stats, dev, handle)
     else:
         compute(X, estar, tau, lo, hi, slab)
-    if world == 1:
+    if world == 1 or not gather:
         return slab
     staged = _host_staged(group) and slab.is_cuda
     src = slab.cpu() if staged else slab
