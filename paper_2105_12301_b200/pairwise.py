@@ -23,7 +23,7 @@ import numpy as np
 from . import _native as nat
 from .embedding import DEFAULT_E_MAX, Dataset, EmbeddingSpec
 from .errors import ParameterError
-from .skill import OptimalEmbedding, lookup_batch, skill_curves
+from .skill import NATIVE_E_MAX, OptimalEmbedding, lookup_batch, skill_curves
 from .tables import build_knn_table
 
 LAYOUT_LIB_MAJOR = 0
@@ -116,6 +116,12 @@ def xmap(values, e_star, tau: int = 1, layout: int = LAYOUT_LIB_MAJOR, dtype=np.
     if tau < 1:
         raise ParameterError(f"tau must be >= 1, got {tau}")
     Xs = np.ascontiguousarray(X.T, dtype=np.float32)  # series-major samples
+    # beyond the fused kernels' formats (E* > NATIVE_E_MAX, or T past the 16-bit
+    # row indices of the table records) the affected pairs take the reference's
+    # composition on the device: build_knn_table + lookup_batch per (library, E)
+    wide = (est > NATIVE_E_MAX) | ((T > NATIVE_T_MAX) & (est > 0))
+    if wide.any():
+        return _xmap_with_wide(Xs, est, wide, tau, layout, dtype, stats)
     out = np.empty((N, N), dtype=np.float32)
     st = np.zeros(8)
     nat.call("cmb_xmap", nat.device(), nat.ptr(Xs), N, T, nat.ptr(est), tau, nat.ptr(out), layout, nat.ptr(st))
@@ -125,6 +131,50 @@ def xmap(values, e_star, tau: int = 1, layout: int = LAYOUT_LIB_MAJOR, dtype=np.
                      pairs=int(st[5]))
     rho = out.T if layout == LAYOUT_TGT_MAJOR else out
     return rho.astype(dtype, copy=False) if dtype != np.float32 else rho
+
+
+NATIVE_T_MAX = 65535  # 16-bit neighbour rows in the cross-map table records (csrc/cmb_common.cuh)
+
+
+def _xmap_with_wide(Xs: np.ndarray, est: np.ndarray, wide: np.ndarray, tau: int, layout: int, dtype,
+                    stats: dict | None) -> np.ndarray:
+    """xmap when some targets are outside the fused kernels' formats.  The fused
+    path runs with those series masked (which also drops them as libraries); the
+    masked libraries' rows for the other targets and every library's column for
+    a wide target are then computed per (library, E) with build_knn_table +
+    lookup_batch (float64 device kernels, ccm.py:131-149 semantics)."""
+    N, T = Xs.shape
+    t0 = time.perf_counter()
+    rho = np.full((N, N), np.nan)
+    est_n = np.where(wide, 0, est).astype(np.int32)
+    st = np.zeros(8)
+    if (est_n > 0).any():
+        out = np.empty((N, N), dtype=np.float32)
+        nat.call("cmb_xmap", nat.device(), nat.ptr(Xs), N, T, nat.ptr(est_n), tau, nat.ptr(out),
+                 LAYOUT_LIB_MAJOR, nat.ptr(st))
+        rho[:] = out
+    narrow: dict = {}
+    far: dict = {}
+    for t in np.flatnonzero(est > 0):
+        (far if wide[t] else narrow).setdefault(int(est[t]), []).append(int(t))
+    X64 = Xs.astype(np.float64)
+    e_top = max(int(est.max()), 1)
+    for lib in np.flatnonzero(est > 0):
+        groups = dict(far)
+        if wide[lib]:
+            for e, ts in narrow.items():
+                groups[e] = groups.get(e, []) + ts
+        for e in sorted(groups):
+            ts = groups[e]
+            table = build_knn_table(X64[lib], EmbeddingSpec(e, tau, e_max=e_top))
+            outs = lookup_batch(table, [X64[t] for t in ts])
+            rho[lib, ts] = [np.nan if o.rho is None else o.rho for o in outs]
+    if stats is not None:
+        stats.update(seconds_table_build=float(st[0]), seconds_lookup=float(st[1]),
+                     seconds_total=time.perf_counter() - t0, tables_built=int(st[3]), distinct_e=int(st[4]),
+                     pairs=int(np.sum(est > 0)) ** 2)
+    out = rho.astype(dtype, copy=False)
+    return np.asfortranarray(out) if layout == LAYOUT_TGT_MAJOR else out
 
 
 def ccm_pairwise(data: Dataset, cfg: CcmConfig | None = None, workers: int | None = None,

@@ -128,6 +128,20 @@ def lookup_batch(table: NeighborTable, targets, want_predictions: bool = False,
     return out  # type: ignore[return-value]
 
 
+# Widest dimension of the fused sweep kernels (CMB_SWEEP_MAX_E in csrc/cmb_common.cuh).
+# Larger E (the reference accepts any e_max) runs the reference's own composition
+# -- build_knn_table + lookup_batch, both device kernels -- one (series, E) at a time.
+NATIVE_E_MAX = 30
+
+
+def _simplex_composed(v: np.ndarray, spec: EmbeddingSpec, tp: int) -> float:
+    """prediction.py:178-179: table on v[:len - tp], lookup of v[tp:]; NaN = undefined."""
+    from .tables import build_knn_table
+    table = build_knn_table(v[: v.size - tp], spec)
+    r = lookup_batch(table, [v[tp:]])[0].rho
+    return float("nan") if r is None else r
+
+
 def simplex_self_predict(series, spec: EmbeddingSpec, tp: int = 1, workers: int | None = None) -> float:
     """Skill of forecasting a series tp steps ahead from its own manifold."""
     v = np.ascontiguousarray(as_values(series))
@@ -137,7 +151,10 @@ def simplex_self_predict(series, spec: EmbeddingSpec, tp: int = 1, workers: int 
         raise SeriesTooShortError(f"series of length {v.size} cannot support horizon {tp}")
     valid_count(v.size - tp, spec)
     rho = np.empty(1)
-    nat.call("cmb_simplex", nat.device(), nat.ptr(v), v.size, spec.E, spec.tau, tp, nat.ptr(rho))
+    if spec.E > NATIVE_E_MAX:
+        rho[0] = _simplex_composed(v, spec, tp)
+    else:
+        nat.call("cmb_simplex", nat.device(), nat.ptr(v), v.size, spec.E, spec.tau, tp, nat.ptr(rho))
     if np.isnan(rho[0]):
         raise ZeroVarianceError("self-prediction skill undefined: constant values over the forecast range")
     return float(rho[0])
@@ -162,8 +179,36 @@ def skill_curves(X: np.ndarray, e_max: int, tau: int, tp: int) -> tuple[np.ndarr
     N, L = X.shape
     rho = np.empty((N, e_max))
     est = np.empty(N, dtype=np.int32)
-    nat.call("cmb_edim", nat.device(), nat.ptr(X), N, L, e_max, tau, tp, nat.ptr(rho), nat.ptr(est))
+    if e_max > NATIVE_E_MAX:
+        _edim_wide(X, e_max, tau, tp, rho, est)
+    else:
+        nat.call("cmb_edim", nat.device(), nat.ptr(X), N, L, e_max, tau, tp, nat.ptr(rho), nat.ptr(est))
     return rho, est
+
+
+def _edim_wide(X: np.ndarray, e_max: int, tau: int, tp: int, rho: np.ndarray, est: np.ndarray) -> None:
+    """skill_curves for e_max > NATIVE_E_MAX: the fused sweep for E <= NATIVE_E_MAX, the
+    reference composition per (series, E) above it, E* re-taken over the whole curve
+    (strict >, ties to the smaller E; undefined when any E is undefined, ccm.py:113-121)."""
+    N, L = X.shape
+    part = np.empty((N, NATIVE_E_MAX))
+    est_dev = np.empty(N, dtype=np.int32)
+    nat.call("cmb_edim", nat.device(), nat.ptr(X), N, L, NATIVE_E_MAX, tau, tp, nat.ptr(part), nat.ptr(est_dev))
+    rho[:, :NATIVE_E_MAX] = part
+    for s in range(N):
+        v = X[s]
+        for E in range(NATIVE_E_MAX + 1, e_max + 1):
+            rho[s, E - 1] = (_simplex_composed(v, EmbeddingSpec(E, tau, e_max=e_max), tp)
+                             if v.min() != v.max() else np.nan)
+        curve = rho[s]
+        if est_dev[s] == 0 or np.isnan(curve).any():
+            est[s] = 0
+            continue
+        best = 0
+        for e in range(1, e_max):
+            if curve[e] > curve[best]:
+                best = e
+        est[s] = best + 1
 
 
 def optimal_embedding(series, e_max: int = DEFAULT_E_MAX, tau: int = 1, tp: int = 1,

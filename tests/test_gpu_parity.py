@@ -376,3 +376,35 @@ def test_xmap_offset_targets():
     r = P.xmap(X.T, ests)
     ref, _ = O.xmap([X[i] for i in range(5)], ests, 1, workers=1)
     assert np.nanmax(np.abs(r - ref)) <= RHO_TOL
+
+
+@pytest.mark.gpu
+def test_wide_dimension_and_long_series_paths(monkeypatch):
+    """E beyond the fused kernels (NATIVE_E_MAX = 30; the reference accepts any
+    e_max) and series past the 16-bit record rows run the reference's own
+    composition (build_knn_table + lookup_batch) on the device."""
+    from paper_2105_12301_b200 import pairwise as PW
+    from paper_2105_12301_b200 import skill as SK
+    x = P.logistic_map(260, r=3.8, v0=0.31).values
+    assert abs(P.simplex_self_predict(x, P.EmbeddingSpec(33, 1, e_max=33)) - O.simplex(x, 33)) <= 1e-10
+    rng = np.random.default_rng(5)
+    X = np.stack([x, rng.random(260), np.sin(np.arange(260) * 0.37) + 0.1 * rng.random(260)])
+    est, curves = P.edim(X.T, 33, 1, 1)
+    for s in range(3):
+        ref = O.skill_curve(X[s], 33)
+        assert np.max(np.abs(curves[s] - np.array([ref[e] for e in range(1, 34)]))) <= 1e-10
+        assert est[s] == O.optimal_e(ref)
+    # cross map with one target at E* = 32 (column and its row via the composition)
+    Xf = rng.random((4, 240)).astype(np.float32).astype(np.float64)
+    ests = [3, 32, 1, 3]
+    r = P.xmap(Xf.T, ests)
+    ref, _ = O.xmap([Xf[i] for i in range(4)], ests)
+    assert np.array_equal(np.isnan(r), np.isnan(ref))
+    assert np.nanmax(np.abs(r - ref)) <= RHO_TOL
+    # the long-series route, exercised at a small length by lowering the bound
+    monkeypatch.setattr(PW, "NATIVE_T_MAX", 100)
+    ests = [2, 1, 4, 2]
+    r = P.xmap(Xf.T, ests, layout=P.LAYOUT_TGT_MAJOR)
+    ref, _ = O.xmap([Xf[i] for i in range(4)], ests)
+    assert np.nanmax(np.abs(r - ref)) <= 1e-9
+    assert SK.NATIVE_E_MAX == 30
