@@ -280,6 +280,150 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
   qglob += ws.total;
 }
 
+// Prediction of one point from its record in a shared-memory stage, resident
+// targets: the arithmetic of warp_libraries' resident path (shift folded into
+// the first operation).
+template <int K>
+__device__ __forceinline__ float rec_predict_res(uint32_t rec, uint32_t tbase, float shift) {
+  constexpr int RO = rec_row_off(K);
+  float wv[2 * ((K + 1) / 2)];
+  uint32_t rv[2 * ((K + 3) / 4)];
+  if constexpr (K == 2) {
+    uint32_t u0;
+    lds_v2(rec, u0, rv[0]);
+    wv[0] = __uint_as_float(u0);
+  } else {
+#pragma unroll
+    for (int c = 0; c < ((rec_implicit(K) ? K - 1 : K) + 1) / 2; ++c) lds_v2(rec + 8 * c, wv[2 * c], wv[2 * c + 1]);
+#pragma unroll
+    for (int c = 0; c < (K + 3) / 4; ++c) lds_v2(rec + RO + 8 * c, rv[2 * c], rv[2 * c + 1]);
+  }
+  if constexpr (rec_implicit(K)) {
+    float yv[K];
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+      yv[kk] = lds_f32(tbase + (row << 7));
+    }
+    float p = __fsub_rn(yv[K - 1], shift);
+#pragma unroll
+    for (int kk = 0; kk < K - 1; ++kk) p = __fmaf_rn(wv[kk], __fsub_rn(yv[kk], yv[K - 1]), p);
+    return p;
+  } else {
+    float p = -shift;
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+      p = __fmaf_rn(wv[kk], lds_f32(tbase + (row << 7)), p);
+    }
+    return p;
+  }
+}
+
+__device__ __forceinline__ float pair_rho(double So, double Soo, bool ocst, double Sp, double Spp, double Sop,
+                                          int n) {
+  const double nn = (double)n;
+  const double m2o = Soo - So * So / nn;
+  const double m2p = Spp - Sp * Sp / nn;
+  const double com = Sop - So * Sp / nn;
+  float r = __int_as_float(0x7fc00000);
+  if (!ocst && m2o > 0.0 && m2p > 0.0) r = (float)fmin(1.0, fmax(-1.0, com / sqrt(m2o * m2p)));
+  return r;
+}
+
+// Two libraries in lockstep (resident targets, small k): each stage slot holds
+// the same record range of libraries l and l + 1 in its two halves, and every
+// point's observed value -- one shared-memory wavefront -- serves both
+// predictions.  For k = 2 (E* = 1, half the targets of the mixed data) that is
+// 7 instead of 8 wavefronts and 29 instead of 34 instructions per point pair.
+// Each library's arithmetic is warp_libraries' (rho differs from the single
+// path only through the fp32 per-stage grouping of the moment sums).
+template <int K>
+__device__ __forceinline__ void warp_library_pairs(const LookupArgs& a, const float* __restrict__ tgt,
+                                                   uint8_t* ring, uint64_t* bars, uint32_t& qglob,
+                                                   int E, int lib0, int npair, int slot_base) {
+  constexpr int R = rec_bytes(K);
+  const int lane = lane_id();
+  const int n = a.T - (E - 1) * a.tau;
+  const int off = (E - 1) * a.tau;
+  const size_t lstride = rec_lib_stride(K, n);
+  const uint8_t* base = a.tab[E] + (size_t)lib0 * lstride;
+  const int half = (a.stage_bytes / 2) & ~15;
+  const int RS = half / R;
+  const int nst = (n + RS - 1) / RS;
+  const int total = npair * nst;
+
+  const int slot = slot_base + lane;
+  const int tgt_id = a.slot_tgt[slot];
+  const double So = a.obs_s[slot], Soo = a.obs_ss[slot];
+  const bool ocst = a.obs_const[slot] != 0;
+  const uint32_t tbase = smem_u32(tgt + lane);
+
+  auto issue = [&](int q, uint8_t* dst, uint64_t* bar) {
+    const int l2 = q / nst, s = q - l2 * nst;
+    const int r0 = s * RS;
+    const int nrec = min(RS, n - r0);
+    const uint32_t bytes = (uint32_t)((nrec * R + 15) & ~15);
+    const uint8_t* src = base + (size_t)(2 * l2) * lstride + (size_t)r0 * R;
+    mbar_expect_tx(bar, 2 * bytes);
+    bulk_g2s(dst, src, bytes, bar);
+    bulk_g2s(dst + half, src + lstride, bytes, bar);
+  };
+  if (lane == 0) {
+    for (int q = 0; q < 2 && q < total; ++q) {
+      const uint32_t g = qglob + q;
+      issue(q, ring + (g & 1) * a.stage_bytes, bars + (g & 1));
+    }
+  }
+  __syncwarp();
+
+  double SpA = 0.0, SppA = 0.0, SopA = 0.0, SpB = 0.0, SppB = 0.0, SopB = 0.0;
+  float shA = 0.f, shB = 0.f;
+  for (int q = 0; q < total; ++q) {
+    const uint32_t g = qglob + q;
+    uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
+    const int l2 = q / nst, s = q - l2 * nst;
+    mbar_wait(bars + (g & 1), (g >> 1) & 1);
+    const uint32_t sA = smem_u32(slotp), sB = sA + half;
+    if (s == 0) {  // per-library shifts (see warp_libraries)
+      shA = rec_predict_res<K>(sA, tbase, 0.f);
+      shB = rec_predict_res<K>(sB, tbase, 0.f);
+    }
+    const int r0 = s * RS;
+    const int nrec = min(RS, n - r0);
+    float spA = 0.f, sppA = 0.f, sopA = 0.f, spB = 0.f, sppB = 0.f, sopB = 0.f;
+#pragma unroll 2
+    for (int r = 0; r < nrec; ++r) {
+      const float o = lds_f32(tbase + ((uint32_t)(off + r0 + r) << 7));
+      const float pA = rec_predict_res<K>(sA + r * R, tbase, shA);
+      const float pB = rec_predict_res<K>(sB + r * R, tbase, shB);
+      spA += pA;
+      sppA = __fmaf_rn(pA, pA, sppA);
+      sopA = __fmaf_rn(o, pA, sopA);
+      spB += pB;
+      sppB = __fmaf_rn(pB, pB, sppB);
+      sopB = __fmaf_rn(o, pB, sopB);
+    }
+    SpA += spA;
+    SppA += sppA;
+    SopA += sopA;
+    SpB += spB;
+    SppB += sppB;
+    SopB += sopB;
+    __syncwarp();
+    if (lane == 0 && q + 2 < total) issue(q + 2, slotp, bars + (g & 1));
+    if (s == nst - 1) {
+      if (tgt_id >= 0) {
+        float* dst = a.rhoT + (size_t)tgt_id * a.ldr;
+        dst[a.lib_col[lib0 + 2 * l2]] = pair_rho(So, Soo, ocst, SpA, SppA, SopA, n);
+        dst[a.lib_col[lib0 + 2 * l2 + 1]] = pair_rho(So, Soo, ocst, SpB, SppB, SopB, n);
+      }
+      SpA = SppA = SopA = SpB = SppB = SopB = 0.0;
+    }
+  }
+  qglob += total;
+}
+
 // fp16-target variant (opt-in, CMB_LOOKUP_FP16=1): the resident block holds 64
 // targets as fp16 scaled to [-1, 1] -- the same 128 bytes per sample row -- and
 // lane l owns targets 2l and 2l + 1, so every shared-memory wavefront (gathers,
@@ -400,6 +544,8 @@ __device__ __forceinline__ void warp_libraries_h16(const LookupArgs& a, const ui
   qglob += ws.total;
 }
 
+constexpr int kPairMaxK = 8;  // library pairs for k <= 8 (register budget)
+
 template <bool RESIDENT, bool H16>
 __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(LookupArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -454,7 +600,11 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
   case kk:                                                                                          \
     if constexpr (H16)                                                                              \
       warp_libraries_h16<kk>(a, reinterpret_cast<const uint8_t*>(tgt), ring, wbars, qglob, E, lib0, nl, blk * 64); \
-    else                                                                                            \
+    else if constexpr (RESIDENT && kk <= kPairMaxK) {                                               \
+      const int np = nl >> 1;                                                                         \
+      if (np) warp_library_pairs<kk>(a, tgt, ring, wbars, qglob, E, lib0, np, blk * 32);            \
+      if (nl & 1) warp_libraries<kk, true>(a, tgt, ring, wbars, qglob, E, lib0 + 2 * np, 1, blk * 32); \
+    } else                                                                                            \
       warp_libraries<kk, RESIDENT>(a, RESIDENT ? tgt : a.Y + (size_t)blk * 32, ring, wbars, qglob, E, lib0, nl, blk * 32); \
     break;
         CMB_K(2) CMB_K(3) CMB_K(4) CMB_K(5) CMB_K(6) CMB_K(7) CMB_K(8) CMB_K(9) CMB_K(10)
