@@ -391,25 +391,23 @@ __device__ __forceinline__ void warp_library_pairs(const LookupArgs& a, const fl
     }
     const int r0 = s * RS;
     const int nrec = min(RS, n - r0);
-    float spA = 0.f, sppA = 0.f, sopA = 0.f, spB = 0.f, sppB = 0.f, sopB = 0.f;
+    // (A, B) moment sums as packed pairs: one FADD2 + two FFMA2 per point
+    float2 sp = make_float2(0.f, 0.f), spp = sp, sop = sp;
 #pragma unroll 2
     for (int r = 0; r < nrec; ++r) {
       const float o = lds_f32(tbase + ((uint32_t)(off + r0 + r) << 7));
-      const float pA = rec_predict_res<K>(sA + r * R, tbase, shA);
-      const float pB = rec_predict_res<K>(sB + r * R, tbase, shB);
-      spA += pA;
-      sppA = __fmaf_rn(pA, pA, sppA);
-      sopA = __fmaf_rn(o, pA, sopA);
-      spB += pB;
-      sppB = __fmaf_rn(pB, pB, sppB);
-      sopB = __fmaf_rn(o, pB, sopB);
+      const float2 p = make_float2(rec_predict_res<K>(sA + r * R, tbase, shA),
+                                   rec_predict_res<K>(sB + r * R, tbase, shB));
+      sp = __fadd2_rn(sp, p);
+      spp = __ffma2_rn(p, p, spp);
+      sop = __ffma2_rn(make_float2(o, o), p, sop);
     }
-    SpA += spA;
-    SppA += sppA;
-    SopA += sopA;
-    SpB += spB;
-    SppB += sppB;
-    SopB += sopB;
+    SpA += sp.x;
+    SppA += spp.x;
+    SopA += sop.x;
+    SpB += sp.y;
+    SppB += spp.y;
+    SopB += sop.y;
     __syncwarp();
     if (lane == 0 && q + 2 < total) issue(q + 2, slotp, bars + (g & 1));
     if (s == nst - 1) {
