@@ -136,9 +136,10 @@ def lookup_alg_wavefronts(estar: np.ndarray, n_libs: int, T: int, tau: int = 1) 
     """Shared-memory wavefronts the lookup issues per step on this rank (the
     binding resource, K3): per embedded point of a (library, 32-target
     block) pair k gathers + the record's 8-byte broadcast loads (ceil(k/2) weight +
-    ceil(k/4) row loads; one load in all for k = 2) + 1 observed-value load.
-    Matched ncu l1tex__data_pipe_lsu_wavefronts_mem_shared within 2%
-    (profiles/r01_lookup_ncu_summary.txt, before the k <= 3 record change)."""
+    ceil(k/4) row loads; one load in all for k = 2) + the observed-value load,
+    shared by the two libraries a warp runs in lockstep (1/2 per pair).  The
+    one-library form matched ncu l1tex__data_pipe_lsu_wavefronts_mem_shared
+    within 2% (profiles/r01_lookup_ncu_summary.txt)."""
     tot = 0.0
     for E in np.unique(estar[estar > 0]):
         NE = int(np.sum(estar == E))
@@ -146,7 +147,7 @@ def lookup_alg_wavefronts(estar: np.ndarray, n_libs: int, T: int, tau: int = 1) 
         k = int(E) + 1
         # record broadcasts: k <= 3 stores k - 1 weights (cmb_common.cuh rec_*)
         rec = 1 if k == 2 else ((k - 1 if k == 3 else k) + 1) // 2 + (k + 3) // 4
-        tot += n_libs * ((NE + 31) // 32) * nE * (k + rec + 1)
+        tot += n_libs * ((NE + 31) // 32) * nE * (k + rec + 0.5)
     return tot
 
 
@@ -432,8 +433,8 @@ def run_ours(args):
                 "bound": "shared-memory wavefronts (the lookup's binding resource)",
                 "achieved": wf / t_look / 1e9, "unit": "G wavefronts/s",
                 "peak": n_sms * sm_clock_ghz(clk), "frac": wf / t_look / 1e9 / (n_sms * sm_clock_ghz(clk)),
-                "wavefronts_per_step": wf, "model": "1 wavefront/clk/SM; k gathers + record broadcasts + 1 "
-                                                    "observed load per point and 32 pairs"},
+                "wavefronts_per_step": wf, "model": "1 wavefront/clk/SM; k gathers + record broadcasts + 1/2 "
+                                                    "observed load (shared by a library pair) per point and 32 pairs"},
             "extra": {"edim_seconds": t_edim, "edim_series_per_s": N / t_edim,
                       "tables_ms_per_step": t_tables_step * 1e3, "lookup_ms_per_step": t_lookup_step * 1e3,
                       "exact_fallback_rows": diag["exact_fallback_rows"], "rows_checked": diag["rows_checked"]},
