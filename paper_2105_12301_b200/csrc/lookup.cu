@@ -280,11 +280,11 @@ __device__ __forceinline__ void warp_libraries(const LookupArgs& a, const float*
   qglob += ws.total;
 }
 
-// Prediction of one point from its record in a shared-memory stage, resident
-// targets: the arithmetic of warp_libraries' resident path (shift folded into
-// the first operation).
-template <int K>
-__device__ __forceinline__ float rec_predict_res(uint32_t rec, uint32_t tbase, float shift) {
+// Prediction of one point from its record in a shared-memory stage: the
+// arithmetic of warp_libraries (shift folded into the first operation); y(row)
+// gathers the lane's target sample (shared memory when resident, else L1/L2).
+template <int K, typename Y>
+__device__ __forceinline__ float rec_predict(uint32_t rec, Y y, float shift) {
   constexpr int RO = rec_row_off(K);
   float wv[2 * ((K + 1) / 2)];
   uint32_t rv[2 * ((K + 3) / 4)];
@@ -301,10 +301,7 @@ __device__ __forceinline__ float rec_predict_res(uint32_t rec, uint32_t tbase, f
   if constexpr (rec_implicit(K)) {
     float yv[K];
 #pragma unroll
-    for (int kk = 0; kk < K; ++kk) {
-      const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
-      yv[kk] = lds_f32(tbase + (row << 7));
-    }
+    for (int kk = 0; kk < K; ++kk) yv[kk] = y(__byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410));
     float p = __fsub_rn(yv[K - 1], shift);
 #pragma unroll
     for (int kk = 0; kk < K - 1; ++kk) p = __fmaf_rn(wv[kk], __fsub_rn(yv[kk], yv[K - 1]), p);
@@ -312,10 +309,7 @@ __device__ __forceinline__ float rec_predict_res(uint32_t rec, uint32_t tbase, f
   } else {
     float p = -shift;
 #pragma unroll
-    for (int kk = 0; kk < K; ++kk) {
-      const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
-      p = __fmaf_rn(wv[kk], lds_f32(tbase + (row << 7)), p);
-    }
+    for (int kk = 0; kk < K; ++kk) p = __fmaf_rn(wv[kk], y(__byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410)), p);
     return p;
   }
 }
@@ -338,7 +332,7 @@ __device__ __forceinline__ float pair_rho(double So, double Soo, bool ocst, doub
 // 7 instead of 8 wavefronts and 29 instead of 34 instructions per point pair.
 // Each library's arithmetic is warp_libraries' (rho differs from the single
 // path only through the fp32 per-stage grouping of the moment sums).
-template <int K>
+template <int K, bool RESIDENT>
 __device__ __forceinline__ void warp_library_pairs(const LookupArgs& a, const float* __restrict__ tgt,
                                                    uint8_t* ring, uint64_t* bars, uint32_t& qglob,
                                                    int E, int lib0, int npair, int slot_base) {
@@ -357,7 +351,13 @@ __device__ __forceinline__ void warp_library_pairs(const LookupArgs& a, const fl
   const int tgt_id = a.slot_tgt[slot];
   const double So = a.obs_s[slot], Soo = a.obs_ss[slot];
   const bool ocst = a.obs_const[slot] != 0;
-  const uint32_t tbase = smem_u32(tgt + lane);
+  const float* __restrict__ tcol = tgt + lane;
+  const int64_t stride = RESIDENT ? 32 : a.ldy;
+  const uint32_t tbase = RESIDENT ? smem_u32(tcol) : 0u;
+  const auto y = [&](uint32_t row) {
+    if constexpr (RESIDENT) return lds_f32(tbase + (row << 7));
+    else return tcol[(int64_t)row * stride];
+  };
 
   auto issue = [&](int q, uint8_t* dst, uint64_t* bar) {
     const int l2 = q / nst, s = q - l2 * nst;
@@ -386,18 +386,19 @@ __device__ __forceinline__ void warp_library_pairs(const LookupArgs& a, const fl
     mbar_wait(bars + (g & 1), (g >> 1) & 1);
     const uint32_t sA = smem_u32(slotp), sB = sA + half;
     if (s == 0) {  // per-library shifts (see warp_libraries)
-      shA = rec_predict_res<K>(sA, tbase, 0.f);
-      shB = rec_predict_res<K>(sB, tbase, 0.f);
+      shA = rec_predict<K>(sA, y, 0.f);
+      shB = rec_predict<K>(sB, y, 0.f);
     }
     const int r0 = s * RS;
     const int nrec = min(RS, n - r0);
     // (A, B) moment sums as packed pairs: one FADD2 + two FFMA2 per point
     float2 sp = make_float2(0.f, 0.f), spp = sp, sop = sp;
-#pragma unroll 2
+    // non-resident gathers come from L2: unroll over points for loads in flight
+    constexpr int UNR = RESIDENT ? 2 : (K <= 3 ? 4 : 2);
+#pragma unroll UNR
     for (int r = 0; r < nrec; ++r) {
-      const float o = lds_f32(tbase + ((uint32_t)(off + r0 + r) << 7));
-      const float2 p = make_float2(rec_predict_res<K>(sA + r * R, tbase, shA),
-                                   rec_predict_res<K>(sB + r * R, tbase, shB));
+      const float o = y((uint32_t)(off + r0 + r));
+      const float2 p = make_float2(rec_predict<K>(sA + r * R, y, shA), rec_predict<K>(sB + r * R, y, shB));
       sp = __fadd2_rn(sp, p);
       spp = __ffma2_rn(p, p, spp);
       sop = __ffma2_rn(make_float2(o, o), p, sop);
@@ -543,6 +544,9 @@ __device__ __forceinline__ void warp_libraries_h16(const LookupArgs& a, const ui
 }
 
 constexpr int kPairMaxK = 31;  // library pairs for every k (A/B: k <= 8 5.83 s, all 5.81 s)
+// non-resident targets (T past shared memory): pairs measured neutral at
+// N = 1,024, T = 10,000 (81.2 vs 80.8 ms, L2-latency-bound gathers), so off
+constexpr int kPairMaxKL2 = 1;
 
 template <bool RESIDENT, bool H16>
 __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(LookupArgs a) {
@@ -598,10 +602,11 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
   case kk:                                                                                          \
     if constexpr (H16)                                                                              \
       warp_libraries_h16<kk>(a, reinterpret_cast<const uint8_t*>(tgt), ring, wbars, qglob, E, lib0, nl, blk * 64); \
-    else if constexpr (RESIDENT && kk <= kPairMaxK) {                                               \
+    else if constexpr (kk <= (RESIDENT ? kPairMaxK : kPairMaxKL2)) {                                \
+      const float* tb = RESIDENT ? tgt : a.Y + (size_t)blk * 32;                                      \
       const int np = nl >> 1;                                                                         \
-      if (np) warp_library_pairs<kk>(a, tgt, ring, wbars, qglob, E, lib0, np, blk * 32);            \
-      if (nl & 1) warp_libraries<kk, true>(a, tgt, ring, wbars, qglob, E, lib0 + 2 * np, 1, blk * 32); \
+      if (np) warp_library_pairs<kk, RESIDENT>(a, tb, ring, wbars, qglob, E, lib0, np, blk * 32);   \
+      if (nl & 1) warp_libraries<kk, RESIDENT>(a, tb, ring, wbars, qglob, E, lib0 + 2 * np, 1, blk * 32); \
     } else                                                                                            \
       warp_libraries<kk, RESIDENT>(a, RESIDENT ? tgt : a.Y + (size_t)blk * 32, ring, wbars, qglob, E, lib0, nl, blk * 32); \
     break;
