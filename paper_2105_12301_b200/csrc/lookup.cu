@@ -325,27 +325,29 @@ __device__ __forceinline__ float pair_rho(double So, double Soo, bool ocst, doub
   return r;
 }
 
-// Two libraries in lockstep (resident targets): each stage slot holds
-// the same record range of libraries l and l + 1 in its two halves, and every
-// point's observed value -- one shared-memory wavefront -- serves both
-// predictions.  For k = 2 (E* = 1, half the targets of the mixed data) that is
-// 7 instead of 8 wavefronts and 29 instead of 34 instructions per point pair.
-// Each library's arithmetic is warp_libraries' (rho differs from the single
-// path only through the fp32 per-stage grouping of the moment sums).
-template <int K, bool RESIDENT>
-__device__ __forceinline__ void warp_library_pairs(const LookupArgs& a, const float* __restrict__ tgt,
+// Libraries in lockstep (resident targets), NL = 2 or 4 at a time: each stage
+// slot holds the same record range of libraries l .. l + NL - 1 in NL parts,
+// and every point's observed value -- one shared-memory wavefront -- serves
+// all NL predictions; the libraries' moment sums are packed FADD2/FFMA2 pairs.
+// For k = 2 (E* = 1, half the targets of the mixed data) pairs take 7 instead
+// of 8 wavefronts and 27.5 instead of 34 instructions per point pair.  Each
+// library's arithmetic is warp_libraries' (rho differs from the single path
+// only through the fp32 per-stage grouping of the moment sums).
+template <int K, bool RESIDENT, int NL>
+__device__ __forceinline__ void warp_library_group(const LookupArgs& a, const float* __restrict__ tgt,
                                                    uint8_t* ring, uint64_t* bars, uint32_t& qglob,
-                                                   int E, int lib0, int npair, int slot_base) {
+                                                   int E, int lib0, int ngroup, int slot_base) {
+  static_assert(NL == 2 || NL == 4, "libraries per group");
   constexpr int R = rec_bytes(K);
   const int lane = lane_id();
   const int n = a.T - (E - 1) * a.tau;
   const int off = (E - 1) * a.tau;
   const size_t lstride = rec_lib_stride(K, n);
   const uint8_t* base = a.tab[E] + (size_t)lib0 * lstride;
-  const int half = (a.stage_bytes / 2) & ~15;
-  const int RS = half / R;
+  const int part = (a.stage_bytes / NL) & ~15;
+  const int RS = part / R;
   const int nst = (n + RS - 1) / RS;
-  const int total = npair * nst;
+  const int total = ngroup * nst;
 
   const int slot = slot_base + lane;
   const int tgt_id = a.slot_tgt[slot];
@@ -360,14 +362,14 @@ __device__ __forceinline__ void warp_library_pairs(const LookupArgs& a, const fl
   };
 
   auto issue = [&](int q, uint8_t* dst, uint64_t* bar) {
-    const int l2 = q / nst, s = q - l2 * nst;
+    const int lg = q / nst, s = q - lg * nst;
     const int r0 = s * RS;
     const int nrec = min(RS, n - r0);
     const uint32_t bytes = (uint32_t)((nrec * R + 15) & ~15);
-    const uint8_t* src = base + (size_t)(2 * l2) * lstride + (size_t)r0 * R;
-    mbar_expect_tx(bar, 2 * bytes);
-    bulk_g2s(dst, src, bytes, bar);
-    bulk_g2s(dst + half, src + lstride, bytes, bar);
+    const uint8_t* src = base + (size_t)(NL * lg) * lstride + (size_t)r0 * R;
+    mbar_expect_tx(bar, NL * bytes);
+#pragma unroll
+    for (int h = 0; h < NL; ++h) bulk_g2s(dst + h * part, src + h * lstride, bytes, bar);
   };
   if (lane == 0) {
     for (int q = 0; q < 2 && q < total; ++q) {
@@ -377,47 +379,58 @@ __device__ __forceinline__ void warp_library_pairs(const LookupArgs& a, const fl
   }
   __syncwarp();
 
-  double SpA = 0.0, SppA = 0.0, SopA = 0.0, SpB = 0.0, SppB = 0.0, SopB = 0.0;
-  float shA = 0.f, shB = 0.f;
+  double Sp[NL], Spp[NL], Sop[NL];
+  float sh[NL];
+#pragma unroll
+  for (int h = 0; h < NL; ++h) Sp[h] = Spp[h] = Sop[h] = 0.0, sh[h] = 0.f;
   for (int q = 0; q < total; ++q) {
     const uint32_t g = qglob + q;
     uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
-    const int l2 = q / nst, s = q - l2 * nst;
+    const int lg = q / nst, s = q - lg * nst;
     mbar_wait(bars + (g & 1), (g >> 1) & 1);
-    const uint32_t sA = smem_u32(slotp), sB = sA + half;
+    const uint32_t s0 = smem_u32(slotp);
     if (s == 0) {  // per-library shifts (see warp_libraries)
-      shA = rec_predict<K>(sA, y, 0.f);
-      shB = rec_predict<K>(sB, y, 0.f);
+#pragma unroll
+      for (int h = 0; h < NL; ++h) sh[h] = rec_predict<K>(s0 + h * part, y, 0.f);
     }
     const int r0 = s * RS;
     const int nrec = min(RS, n - r0);
-    // (A, B) moment sums as packed pairs: one FADD2 + two FFMA2 per point
-    float2 sp = make_float2(0.f, 0.f), spp = sp, sop = sp;
+    float2 sp[NL / 2], spp[NL / 2], sop[NL / 2];
+#pragma unroll
+    for (int h = 0; h < NL / 2; ++h) sp[h] = spp[h] = sop[h] = make_float2(0.f, 0.f);
     // non-resident gathers come from L2: unroll over points for loads in flight
     constexpr int UNR = RESIDENT ? 2 : (K <= 3 ? 4 : 2);
 #pragma unroll UNR
     for (int r = 0; r < nrec; ++r) {
       const float o = y((uint32_t)(off + r0 + r));
-      const float2 p = make_float2(rec_predict<K>(sA + r * R, y, shA), rec_predict<K>(sB + r * R, y, shB));
-      sp = __fadd2_rn(sp, p);
-      spp = __ffma2_rn(p, p, spp);
-      sop = __ffma2_rn(make_float2(o, o), p, sop);
+#pragma unroll
+      for (int h = 0; h < NL / 2; ++h) {
+        const float2 p = make_float2(rec_predict<K>(s0 + (2 * h) * part + r * R, y, sh[2 * h]),
+                                     rec_predict<K>(s0 + (2 * h + 1) * part + r * R, y, sh[2 * h + 1]));
+        sp[h] = __fadd2_rn(sp[h], p);
+        spp[h] = __ffma2_rn(p, p, spp[h]);
+        sop[h] = __ffma2_rn(make_float2(o, o), p, sop[h]);
+      }
     }
-    SpA += sp.x;
-    SppA += spp.x;
-    SopA += sop.x;
-    SpB += sp.y;
-    SppB += spp.y;
-    SopB += sop.y;
+#pragma unroll
+    for (int h = 0; h < NL / 2; ++h) {
+      Sp[2 * h] += sp[h].x;
+      Spp[2 * h] += spp[h].x;
+      Sop[2 * h] += sop[h].x;
+      Sp[2 * h + 1] += sp[h].y;
+      Spp[2 * h + 1] += spp[h].y;
+      Sop[2 * h + 1] += sop[h].y;
+    }
     __syncwarp();
     if (lane == 0 && q + 2 < total) issue(q + 2, slotp, bars + (g & 1));
     if (s == nst - 1) {
       if (tgt_id >= 0) {
         float* dst = a.rhoT + (size_t)tgt_id * a.ldr;
-        dst[a.lib_col[lib0 + 2 * l2]] = pair_rho(So, Soo, ocst, SpA, SppA, SopA, n);
-        dst[a.lib_col[lib0 + 2 * l2 + 1]] = pair_rho(So, Soo, ocst, SpB, SppB, SopB, n);
+#pragma unroll
+        for (int h = 0; h < NL; ++h) dst[a.lib_col[lib0 + NL * lg + h]] = pair_rho(So, Soo, ocst, Sp[h], Spp[h], Sop[h], n);
       }
-      SpA = SppA = SopA = SpB = SppB = SopB = 0.0;
+#pragma unroll
+      for (int h = 0; h < NL; ++h) Sp[h] = Spp[h] = Sop[h] = 0.0;
     }
   }
   qglob += total;
@@ -547,6 +560,7 @@ constexpr int kPairMaxK = 31;  // library pairs for every k (A/B: k <= 8 5.83 s,
 // non-resident targets (T past shared memory): pairs measured neutral at
 // N = 1,024, T = 10,000 (81.2 vs 80.8 ms, L2-latency-bound gathers), so off
 constexpr int kPairMaxKL2 = 1;
+constexpr int kQuadMaxK = 4;  // four libraries in lockstep for k <= 4
 
 template <bool RESIDENT, bool H16>
 __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(LookupArgs a) {
@@ -604,9 +618,16 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
       warp_libraries_h16<kk>(a, reinterpret_cast<const uint8_t*>(tgt), ring, wbars, qglob, E, lib0, nl, blk * 64); \
     else if constexpr (kk <= (RESIDENT ? kPairMaxK : kPairMaxKL2)) {                                \
       const float* tb = RESIDENT ? tgt : a.Y + (size_t)blk * 32;                                      \
-      const int np = nl >> 1;                                                                         \
-      if (np) warp_library_pairs<kk, RESIDENT>(a, tb, ring, wbars, qglob, E, lib0, np, blk * 32);   \
-      if (nl & 1) warp_libraries<kk, RESIDENT>(a, tb, ring, wbars, qglob, E, lib0 + 2 * np, 1, blk * 32); \
+      int l = 0;                                                                                      \
+      if constexpr (kk <= kQuadMaxK) {                                                                \
+        const int nq = nl >> 2;                                                                       \
+        if (nq) warp_library_group<kk, RESIDENT, 4>(a, tb, ring, wbars, qglob, E, lib0, nq, blk * 32); \
+        l = 4 * nq;                                                                                   \
+      }                                                                                               \
+      const int np = (nl - l) >> 1;                                                                   \
+      if (np) warp_library_group<kk, RESIDENT, 2>(a, tb, ring, wbars, qglob, E, lib0 + l, np, blk * 32); \
+      l += 2 * np;                                                                                    \
+      if (l < nl) warp_libraries<kk, RESIDENT>(a, tb, ring, wbars, qglob, E, lib0 + l, 1, blk * 32);  \
     } else                                                                                            \
       warp_libraries<kk, RESIDENT>(a, RESIDENT ? tgt : a.Y + (size_t)blk * 32, ring, wbars, qglob, E, lib0, nl, blk * 32); \
     break;
