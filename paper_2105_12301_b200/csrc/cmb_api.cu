@@ -252,7 +252,9 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   int e_hi = 0, max_rec = 0;
   // opt-in fp16 target blocks (64 targets per block, lookup.cu warp_libraries_h16)
   const char* h16_env = getenv("CMB_LOOKUP_FP16");
-  const bool want_h16 = h16_env && h16_env[0] == '1';
+  // (CMB_LOOKUP_FP16=2: 16-bit fixed point instead of fp16, same layout)
+  const int h16_mode = h16_env && (h16_env[0] == '1' || h16_env[0] == '2') ? h16_env[0] - '0' : 0;
+  const bool want_h16 = h16_mode != 0;
   const int blk_sz = want_h16 ? 64 : 32;
   for (int e = 1; e <= CMB_SWEEP_MAX_E; ++e) {
     if (by_e[e].empty()) continue;
@@ -315,7 +317,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     CMB_CUDA(ctx->buf[B_YH].ensure(2 * T * ldy));
     CMB_CUDA(launch_targets_to_half(ctx->buf[B_Y].as<float>(), ldy, (int)T, tau, ctx->buf[B_SLOT_E].as<int32_t>(),
                                     slots, ctx->buf[B_YH].p, ctx->buf[B_OBS_S].as<double>(),
-                                    ctx->buf[B_OBS_SS].as<double>(), ctx->buf[B_OBS_C].as<uint8_t>(), st));
+                                    ctx->buf[B_OBS_SS].as<double>(), ctx->buf[B_OBS_C].as<uint8_t>(), h16_mode, st));
   } else {
     CMB_CUDA(launch_obs_moments(ctx->buf[B_Y].as<float>(), ldy, (int)T, tau, ctx->buf[B_SLOT_E].as<int32_t>(),
                                 slots, ctx->buf[B_OBS_S].as<double>(), ctx->buf[B_OBS_SS].as<double>(),
@@ -372,7 +374,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     CMB_CUDA(cudaEventRecord(ev[1], st));
 
     la.Y = h16 ? reinterpret_cast<const float*>(ctx->buf[B_YH].p) : ctx->buf[B_Y].as<float>();
-    la.h16 = h16 ? 1 : 0;
+    la.h16 = h16 ? h16_mode : 0;
     la.ldy = ldy;
     la.T = (int)T;
     la.tau = tau;

@@ -73,7 +73,7 @@ struct LookupArgs {
   float* rhoT;               // rho_T[tgt * ldr + col]
   int64_t ldr;
   int stage_bytes;           // per-warp table staging slot
-  int h16;                   // targets are fp16 (Y holds __half), 64 per block, two per lane
+  int h16;                   // 16-bit targets, 64 per block, two per lane: 1 fp16, 2 q16 fixed point
 };
 
 constexpr int kLookupWarps = 16;
@@ -97,7 +97,7 @@ cudaError_t launch_obs_moments(const float* Y, int64_t ldy, int T, int tau, cons
 cudaError_t launch_fill_nan(float* p, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
 cudaError_t launch_targets_to_half(const float* Y, int64_t ldy, int T, int tau, const int32_t* slot_E,
                                    int64_t slots, void* Yh, double* s, double* ss, uint8_t* cst,
-                                   cudaStream_t st);
+                                   int mode, cudaStream_t st);
 cudaError_t launch_pairwise(const double* x, int n, int E, int tau, double* D, cudaStream_t st);
 cudaError_t launch_topk_rows(const double* D, int n, int k, double* d_out, int64_t* i_out,
                              cudaStream_t st);

@@ -85,6 +85,23 @@ __device__ __forceinline__ float2 h2f2(uint32_t u) {
   return __half22float2(h);
 }
 
+// 16-bit target words (two targets per lane): raw values whose differences are
+// exact, and debias() to the value itself.  MODE 1: fp16.  MODE 2 (q16): each
+// biased u16 is placed under the exponent of 2^23 by one PRMT, i.e. the float
+// 2^23 + 32768 + v, so differences of raw values are exact integers.
+template <int MODE>
+__device__ __forceinline__ float2 t16_raw(uint32_t u) {
+  if constexpr (MODE == 1) return h2f2(u);
+  else
+    return make_float2(__uint_as_float(__byte_perm(u, 0x4B000000u, 0x7610)),
+                       __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7632)));
+}
+template <int MODE>
+__device__ __forceinline__ float2 t16_debias(float2 f) {
+  if constexpr (MODE == 1) return f;
+  else return __fadd2_rn(f, make_float2(-8421376.f, -8421376.f));
+}
+
 __device__ __forceinline__ void lds_v2(uint32_t addr, float& x, float& y) {
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(x), "=f"(y) : "r"(addr));
 }
@@ -441,7 +458,7 @@ __device__ __forceinline__ void warp_library_group(const LookupArgs& a, const fl
 // lane l owns targets 2l and 2l + 1, so every shared-memory wavefront (gathers,
 // record broadcasts, observed values) serves 64 pairs instead of 32.  Values are
 // widened to fp32 and accumulated with packed FFMA2; rho as in the fp32 path.
-template <int K>
+template <int K, int MODE>
 __device__ __forceinline__ void warp_libraries_h16(const LookupArgs& a, const uint8_t* tgt,
                                                    uint8_t* ring, uint64_t* bars, uint32_t& qglob,
                                                    int E, int lib0, int nl, int slot_base) {
@@ -480,55 +497,68 @@ __device__ __forceinline__ void warp_libraries_h16(const LookupArgs& a, const ui
   }
   __syncwarp();
 
+  // prediction of one point from its record (debiased values); the moments
+  // are accumulated about the library's first prediction as in warp_libraries
+  const auto predict = [&](uint32_t rec) {
+    float wv[2 * ((K + 1) / 2)];
+    uint32_t rv[2 * ((K + 3) / 4)];
+    if constexpr (K == 2) {
+      uint32_t u0;
+      lds_v2(rec, u0, rv[0]);
+      wv[0] = __uint_as_float(u0);
+    } else {
+#pragma unroll
+      for (int c = 0; c < ((rec_implicit(K) ? K - 1 : K) + 1) / 2; ++c)
+        lds_v2(rec + 8 * c, wv[2 * c], wv[2 * c + 1]);
+#pragma unroll
+      for (int c = 0; c < (K + 3) / 4; ++c) lds_v2(rec + RO + 8 * c, rv[2 * c], rv[2 * c + 1]);
+    }
+    float2 p;
+    if constexpr (rec_implicit(K)) {
+      float2 yv[K];
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+        yv[kk] = t16_raw<MODE>(lds_u32(tbase + (row << 7)));
+      }
+      p = t16_debias<MODE>(yv[K - 1]);
+#pragma unroll
+      for (int kk = 0; kk < K - 1; ++kk) {
+        const float2 d = make_float2(__fsub_rn(yv[kk].x, yv[K - 1].x), __fsub_rn(yv[kk].y, yv[K - 1].y));
+        p = __ffma2_rn(make_float2(wv[kk], wv[kk]), d, p);
+      }
+    } else {
+      p = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int kk = 0; kk < K; ++kk) {
+        const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
+        p = __ffma2_rn(make_float2(wv[kk], wv[kk]), t16_debias<MODE>(t16_raw<MODE>(lds_u32(tbase + (row << 7)))), p);
+      }
+    }
+    return p;
+  };
+
   double Sp0 = 0, Sp1 = 0, Spp0 = 0, Spp1 = 0, Sop0 = 0, Sop1 = 0;
+  float2 nshift = make_float2(0.f, 0.f);
   for (int q = 0; q < ws.total; ++q) {
     const uint32_t g = qglob + q;
     uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
     mbar_wait(bars + (g & 1), (g >> 1) & 1);
     const uint32_t slot_s = smem_u32(slotp);
     const int l = q / ws.nst, s = q - l * ws.nst;
+    if (s == 0) {
+      const float2 f = predict(slot_s);
+      nshift = make_float2(-f.x, -f.y);
+    }
     const int r0 = s * ws.RS;
     const int nrec = min(ws.RS, n - r0);
     float2 sp = make_float2(0.f, 0.f), spp = sp, sop = sp;
 #pragma unroll 2
     for (int r = 0; r < nrec; ++r) {
-      const uint32_t rec = slot_s + r * R;
-      float wv[2 * ((K + 1) / 2)];
-      uint32_t rv[2 * ((K + 3) / 4)];
-      if constexpr (K == 2) {
-        uint32_t u0;
-        lds_v2(rec, u0, rv[0]);
-        wv[0] = __uint_as_float(u0);
-      } else {
-#pragma unroll
-        for (int c = 0; c < ((rec_implicit(K) ? K - 1 : K) + 1) / 2; ++c)
-          lds_v2(rec + 8 * c, wv[2 * c], wv[2 * c + 1]);
-#pragma unroll
-        for (int c = 0; c < (K + 3) / 4; ++c) lds_v2(rec + RO + 8 * c, rv[2 * c], rv[2 * c + 1]);
-      }
-      const float2 o = h2f2(lds_u32(tbase + ((uint32_t)(off + r0 + r) << 7)));
-      float2 p;
-      if constexpr (rec_implicit(K)) {
-        float2 yv[K];
-#pragma unroll
-        for (int kk = 0; kk < K; ++kk) {
-          const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
-          yv[kk] = h2f2(lds_u32(tbase + (row << 7)));
-        }
-        p = yv[K - 1];
-#pragma unroll
-        for (int kk = 0; kk < K - 1; ++kk) {
-          const float2 d = make_float2(__fsub_rn(yv[kk].x, yv[K - 1].x), __fsub_rn(yv[kk].y, yv[K - 1].y));
-          p = __ffma2_rn(make_float2(wv[kk], wv[kk]), d, p);
-        }
-      } else {
-        p = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int kk = 0; kk < K; ++kk) {
-          const uint32_t row = __byte_perm(rv[kk >> 1], 0, (kk & 1) ? 0x4432 : 0x4410);
-          p = __ffma2_rn(make_float2(wv[kk], wv[kk]), h2f2(lds_u32(tbase + (row << 7))), p);
-        }
-      }
+      const float2 o = t16_debias<MODE>(t16_raw<MODE>(lds_u32(tbase + ((uint32_t)(off + r0 + r) << 7))));
+      // the shift is subtracted from the complete prediction, so a prediction
+      // equal to the library's first one contributes exactly zero
+      const float2 p = __fadd2_rn(predict(slot_s + r * R), nshift);
       sp = __fadd2_rn(sp, p);
       spp = __ffma2_rn(p, p, spp);
       sop = __ffma2_rn(o, p, sop);
@@ -562,7 +592,7 @@ constexpr int kPairMaxK = 31;  // library pairs for every k (A/B: k <= 8 5.83 s,
 constexpr int kPairMaxKL2 = 1;
 constexpr int kQuadMaxK = 4;  // four libraries in lockstep for k <= 4
 
-template <bool RESIDENT, bool H16>
+template <bool RESIDENT, int H16>
 __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(LookupArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   float* tgt = reinterpret_cast<float*>(smem);
@@ -615,7 +645,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
 #define CMB_K(kk)                                                                                   \
   case kk:                                                                                          \
     if constexpr (H16)                                                                              \
-      warp_libraries_h16<kk>(a, reinterpret_cast<const uint8_t*>(tgt), ring, wbars, qglob, E, lib0, nl, blk * 64); \
+      warp_libraries_h16<kk, H16>(a, reinterpret_cast<const uint8_t*>(tgt), ring, wbars, qglob, E, lib0, nl, blk * 64); \
     else if constexpr (kk <= (RESIDENT ? kPairMaxK : kPairMaxKL2)) {                                \
       const float* tb = RESIDENT ? tgt : a.Y + (size_t)blk * 32;                                      \
       int l = 0;                                                                                      \
@@ -660,8 +690,10 @@ int lookup_stage_bytes(int T, int max_rec_bytes) {
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st) {
   const bool resident = a.stage_bytes != kNonResidentStage;
   const int smem = (resident ? a.T * 128 : 0) + kLookupWarps * 2 * a.stage_bytes + kLookupWarps * 2 * 8;
-  auto kern = !resident ? lookup_xmap_kernel<false, false>
-                        : (a.h16 ? lookup_xmap_kernel<true, true> : lookup_xmap_kernel<true, false>);
+  auto kern = !resident      ? lookup_xmap_kernel<false, 0>
+              : a.h16 == 2 ? lookup_xmap_kernel<true, 2>
+              : a.h16      ? lookup_xmap_kernel<true, 1>
+                           : lookup_xmap_kernel<true, 0>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
   count_launch();

@@ -113,22 +113,42 @@ __global__ void obs_moments_kernel(const float* __restrict__ Y, int64_t ldy, int
 __global__ void targets_to_half_kernel(const float* __restrict__ Y, int64_t ldy, int T, int tau,
                                        const int32_t* __restrict__ slot_E, int64_t slots,
                                        __half* __restrict__ Yh, double* __restrict__ s1,
-                                       double* __restrict__ s2, uint8_t* __restrict__ cst) {
+                                       double* __restrict__ s2, uint8_t* __restrict__ cst, int mode) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= slots) return;
-  float m = 0.f;
-  for (int t = 0; t < T; ++t) m = fmaxf(m, fabsf(Y[(int64_t)t * ldy + s]));
-  const float inv = (m > 0.f) ? 1.f / m : 1.f;
-  for (int t = 0; t < T; ++t) Yh[(int64_t)t * ldy + s] = __float2half_rn(Y[(int64_t)t * ldy + s] * inv);
+  float m = 0.f, mn = INFINITY, mx = -INFINITY;
+  for (int t = 0; t < T; ++t) {
+    const float y = Y[(int64_t)t * ldy + s];
+    m = fmaxf(m, fabsf(y));
+    mn = fminf(mn, y);
+    mx = fmaxf(mx, y);
+  }
+  // mode 2 (q16): signed 16-bit fixed point v = rint((y - mid) * 32767 / half
+  // range) over the full [-32767, 32767] (rho is invariant to the affine map),
+  // stored biased by 32768 so the lookup rebuilds 2^23 + 32768 + v with one PRMT
+  const float mid = mode == 2 ? 0.5f * (mn + mx) : 0.f;
+  if (mode == 2) m = 0.5f * (mx - mn);
+  const float inv = (m > 0.f) ? (mode == 2 ? 32767.f : 1.f) / m : 1.f;
+  uint16_t* Yq = reinterpret_cast<uint16_t*>(Yh);
+  const auto rd = [&](int64_t t) {
+    return mode == 2 ? (float)((int)Yq[t * ldy + s] - 32768) : __half2float(Yh[t * ldy + s]);
+  };
+  for (int t = 0; t < T; ++t) {
+    const float y = (Y[(int64_t)t * ldy + s] - mid) * inv;
+    if (mode == 2)
+      Yq[(int64_t)t * ldy + s] = (uint16_t)((int)fminf(32767.f, fmaxf(-32767.f, rintf(y))) + 32768);
+    else
+      Yh[(int64_t)t * ldy + s] = __float2half_rn(y);
+  }
   const int E = slot_E[s];
   if (E <= 0) { s1[s] = 0; s2[s] = 0; cst[s] = 1; return; }
   const int off = (E - 1) * tau;
   const int n = T - off;
   double a = 0.0, b = 0.0;
-  const float first = __half2float(Yh[(int64_t)off * ldy + s]);
+  const float first = rd(off);
   bool c = true;
   for (int t = 0; t < n; ++t) {
-    const float v = __half2float(Yh[(int64_t)(off + t) * ldy + s]);
+    const float v = rd(off + t);
     a += (double)v;
     b += (double)v * (double)v;
     c = c && (v == first);
@@ -378,11 +398,11 @@ cudaError_t launch_obs_moments(const float* Y, int64_t ldy, int T, int tau, cons
 
 cudaError_t launch_targets_to_half(const float* Y, int64_t ldy, int T, int tau, const int32_t* slot_E,
                                    int64_t slots, void* Yh, double* s, double* ss, uint8_t* cst,
-                                   cudaStream_t st) {
+                                   int mode, cudaStream_t st) {
   if (slots == 0) return cudaSuccess;
   count_launch();
   targets_to_half_kernel<<<(unsigned)((slots + 127) / 128), 128, 0, st>>>(
-      Y, ldy, T, tau, slot_E, slots, reinterpret_cast<__half*>(Yh), s, ss, cst);
+      Y, ldy, T, tau, slot_E, slots, reinterpret_cast<__half*>(Yh), s, ss, cst, mode);
   return cudaGetLastError();
 }
 
