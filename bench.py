@@ -345,10 +345,14 @@ def run_ours(args):
             diff = torch.nan_to_num(torch.abs(ref - got), nan=0.0)
             dmax = float(diff.max())
             n_over = int((diff > 1e-4).sum())
+            wt, wl = divmod(int(torch.argmax(diff)), diff.shape[1])  # slab is rho_T[tgt][lib]
+            worst = {"lib": wl, "tgt": wt, "rho_fp32": float(ref[wt, wl]), "rho_mode": float(got[wt, wl]),
+                     "E_tgt": int(estar[wt]), "E_lib": int(estar[wl])}
             fp16["fp16" if mode == "1" else "q16"] = {
                 "env": f"CMB_LOOKUP_FP16={mode}", "value": pairs / (ms16 * 1e-3), "ms_per_step": ms16,
                 "lookup_ms_per_step": t16 * 1e3, "roofline_frac_hbm": alg / t16 / 1e9 / peak,
                 "max_abs_rho_diff_vs_fp32": dmax, "pairs_over_1e-4": n_over, "nan_pattern_equal": same_nan,
+                "worst_pair": worst,
                 "note": notes.get(mode, "") + "; opt-in, not the headline"}
             del got, diff
         del ref
