@@ -332,7 +332,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     const int e = la.g_E[g];
     per_lib += rec_lib_stride(e + 1, T - (int64_t)(e - 1) * tau);
   }
-  const int LS = 64;
+  const int LS = 4 * kLookupWarps;  // four libraries per warp per work item
   const size_t budget = (size_t)6 << 30;
   int64_t C = (int64_t)(budget / std::max<size_t>(per_lib, 1));
   C = std::max<int64_t>(LS, C / LS * LS);
@@ -834,7 +834,7 @@ int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E,
   CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_SLOT_TGT].p, slot_row.data(), 4 * slots, cudaMemcpyHostToDevice, st));
   // chunks of pseudo-libraries: tables (<= ~4 GB) and their rho_T columns
   const size_t stride = rec_lib_stride(k, n);
-  const int LS = 64;
+  const int LS = 4 * kLookupWarps;  // four libraries per warp per work item
   int64_t C = std::max<int64_t>(LS, (int64_t)(((size_t)4 << 30) / stride) / LS * LS);
   C = std::min<int64_t>(C, (PL + LS - 1) / LS * LS);
   const int64_t ldr = (C + 3) / 4 * 4;
