@@ -293,9 +293,10 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
 
   const double M = a.err_m ? (double)a.err_m[lib] : 0.0;
   const int e_hi = a.e_hi;
-  const int rpw = (a.rows_per_block + kWarps - 1) / kWarps;
-  const int r0 = rb * a.rows_per_block + w * rpw;
-  const int r1 = min(min(L, rb * a.rows_per_block + a.rows_per_block), r0 + rpw);
+  // rows interleaved over the warps (no state carries between rows), so the
+  // last, partial block of a library keeps all eight warps busy
+  const int r0 = rb * a.rows_per_block + w;
+  const int r1 = min(L, rb * a.rows_per_block + a.rows_per_block);
   Entry* wl = lists + w * LT;
   Entry* wb = bufs + w * E_HI * kCap;
   float* wscr = scratch + w * kScrWarp;
@@ -305,7 +306,7 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
   double acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0, acc4 = 0;
   const double shift = (a.mode == KNN_EDIM) ? s_mean : 0.0;
 
-  for (int i = r0; i < r1; ++i) {
+  for (int i = r0; i < r1; i += kWarps) {
     uint32_t act = 0;
     for (int e = 0; e < e_hi; ++e)
       if (((a.need >> e) & 1u) && i < L - e) act |= 1u << e;
