@@ -10,9 +10,15 @@ HBM (tables + lookup; for N > 1 also the NCCL broadcast of X and the gather of
 rho slabs to rank 0).  X (308 MB) and rho (11.3 GB) exceed the 126 MB L2, so
 no flush is needed between steps.
 
-``--impl reference`` times the CPU oracle (oracle/crossmap_oracle.py, a
-restatement of the reference's numpy algorithm; the reference is pure Python
-and cannot ship to the GPU box) on a bounded sample of the same workload.
+``--impl reference`` times the reference's own CPU implementation -- the
+unmodified ``crossmap`` package installed in baseline/_ref (git-ignored, shipped
+to the GPU box), its stock ``build_knn_table`` + ``lookup_batch`` loop body of
+``ccm_pairwise`` (pkg/src/crossmap/ccm.py:131-149) with every host core -- one
+whole library row per step, a different library each step, under the E* of
+tests/golden/estar_config3.npz; it never loads libcmb200.so.  Without
+baseline/_ref it times the oracle restatement (oracle/crossmap_oracle.py).
+The GPU arm's ``cpu_baseline`` runs the same stock path on >= 3 random rows and
+compares them with the GPU rho of its last timed step (``parity``).
 """
 
 from __future__ import annotations
@@ -45,7 +51,7 @@ def parse():
     p.add_argument("--length", dest="t", type=int, default=1450)
     p.add_argument("--seed", type=int, default=2105)
     p.add_argument("--e-max", type=int, default=20)
-    p.add_argument("--cpu-seconds", type=float, default=15.0, help="CPU baseline sample budget")
+    p.add_argument("--cpu-seconds", type=float, default=20.0, help="CPU baseline sample budget (>= 3 rows)")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--lookup-fp16", nargs="?", const="1", default=None,
@@ -158,67 +164,161 @@ def make_data(n, t, seed):
 
 
 # ---------------------------------------------------------------- CPU arm
-def cpu_sample(X: np.ndarray, estar: np.ndarray, budget_s: float, workers: int):
-    """Oracle xmap on whole library rows (all targets) until the budget is spent."""
-    sys.path.insert(0, str(ROOT / "oracle"))
-    import crossmap_oracle as O
-    series = [X[i].astype(np.float64) for i in range(X.shape[0])]
+ESTAR_FIXTURE = ROOT / "tests" / "golden" / "estar_config3.npz"
+
+
+def reference_package():
+    """The unmodified reference package ``crossmap`` installed in baseline/_ref
+    (pip --target), or None when it is not there."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "crossmap" / "__init__.py").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    import crossmap
+    return crossmap
+
+
+def fixture_estar(n, t, seed):
+    """E* of the config-3 dataset (GPU edim, E_max = 20, Tp = 1) as committed in
+    tests/golden/estar_config3.npz; None for other shapes."""
+    if not ESTAR_FIXTURE.exists():
+        return None
+    d = np.load(ESTAR_FIXTURE)
+    if (int(d["n"]), int(d["t"]), int(d["seed"])) != (n, t, seed):
+        return None
+    return d["estar"].astype(np.int32)
+
+
+class StockRows:
+    """Whole library rows of the cross map through the reference's stock CPU
+    path: per library, for every E group, ``build_knn_table`` + ``lookup_batch``
+    (pkg/src/crossmap/ccm.py:131-149, the loop body of ccm_pairwise) from the
+    unmodified package in baseline/_ref, with every host core.  Falls back to
+    the oracle restatement (oracle/crossmap_oracle.py) when the package is
+    absent.  Setup (validated series objects, E groups) is done once, untimed."""
+
+    def __init__(self, X: np.ndarray, estar: np.ndarray, tau: int = 1):
+        self.N = X.shape[0]
+        self.tau = tau
+        self.workers = os.cpu_count() or 1
+        self.estar = estar
+        self.groups = {}
+        for t, e in enumerate(estar):
+            if e > 0:
+                self.groups.setdefault(int(e), []).append(t)
+        self.cm = reference_package()
+        self.kind = "reference" if self.cm is not None else "port"
+        if self.cm is not None:
+            TS = self.cm.TimeSeries
+            self.series = [TS(X[i].astype(np.float64), name=f"s{i}") for i in range(self.N)]
+            self.tgt = {e: [self.series[t] for t in ids] for e, ids in self.groups.items()}
+        else:
+            sys.path.insert(0, str(ROOT / "oracle"))
+            import crossmap_oracle as O
+            self.O = O
+            self.series = [X[i].astype(np.float64) for i in range(self.N)]
+
+    def row(self, lib: int) -> np.ndarray:
+        out = np.full(self.N, np.nan)
+        if self.estar[lib] <= 0:
+            return out
+        if self.cm is None:
+            return self.O.xmap_rows(self.series, [int(e) for e in self.estar], [lib], self.tau,
+                                    workers=self.workers)[0]
+        cm = self.cm
+        for e in sorted(self.groups):
+            table = cm.build_knn_table(self.series[lib], cm.EmbeddingSpec(e, self.tau), workers=self.workers)
+            outs = cm.lookup_batch(table, self.tgt[e], workers=self.workers)
+            for t, o in zip(self.groups[e], outs):
+                if o.rho is not None:
+                    out[t] = o.rho
+        return out
+
+
+def cpu_sample(X: np.ndarray, estar: np.ndarray, budget_s: float, seed: int = 0, min_rows: int = 1):
+    """Stock CPU rows for random libraries until the budget is spent (at least
+    ``min_rows``).  Returns (pairs/s, sample text, seconds, libs, rows, kind)."""
+    stock = StockRows(X, estar)
     valid = np.flatnonzero(estar > 0)
-    rng = np.random.default_rng(0)
-    libs = rng.permutation(valid)
-    done_pairs = 0
+    libs = np.random.default_rng(seed).permutation(valid)
+    rows, done = [], []
     t0 = time.perf_counter()
-    n_libs = 0
     for lib in libs:
-        O.xmap(series, [int(e) for e in estar], 1, workers=workers, libraries=[int(lib)])
-        done_pairs += valid.size
-        n_libs += 1
-        if time.perf_counter() - t0 >= budget_s:
+        rows.append(stock.row(int(lib)))
+        done.append(int(lib))
+        if time.perf_counter() - t0 >= budget_s and len(done) >= min_rows:
             break
     el = time.perf_counter() - t0
-    return done_pairs / el, f"{n_libs} random libraries x all {valid.size} targets (oracle xmap rows)", el
+    pairs = len(done) * valid.size
+    text = (f"{len(done)} random libraries x all {valid.size} targets "
+            f"({'baseline/_ref crossmap build_knn_table + lookup_batch' if stock.kind == 'reference' else 'oracle port'}"
+            f", {stock.workers} threads)")
+    return pairs / el, text, el, done, np.stack(rows), stock.kind
 
 
 def run_reference(args):
+    """--impl reference: the reference's own CPU implementation of the path on
+    the box's host cores, one library row per step (a different library every
+    step), never loading libcmb200.so."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     X = make_data(args.n, args.t, args.seed)
-    estar = cpu_estar(X, args)
-    workers = os.cpu_count() or 1
-    vals = []
-    samples = ""
-    for _ in range(args.warmup):
-        cpu_sample(X, estar, min(3.0, args.cpu_seconds), workers)
-    for _ in range(args.steps):
-        v, samples, _ = cpu_sample(X, estar, args.cpu_seconds / max(1, args.steps), workers)
-        vals.append(v)
-    v = float(np.mean(vals))
-    n_pairs = float(np.sum(estar > 0)) ** 2
+    estar = fixture_estar(args.n, args.t, args.seed)
+    estar_src = "tests/golden/estar_config3.npz (GPU edim, E_max=20, Tp=1)"
+    stock = None
+    if estar is None:
+        cm = reference_package()
+        if cm is None:
+            print(json.dumps({"impl": "reference", "unavailable": "baseline/_ref missing and no E* fixture "
+                              "for this shape"}), flush=True)
+            return
+        # the reference's own edim (prediction.py:243-262) for small shapes
+        estar = np.zeros(args.n, np.int32)
+        for i in range(args.n):
+            try:
+                estar[i] = cm.optimal_embedding(X[i].astype(np.float64), args.e_max, 1, 1).e_star
+            except cm.ZeroVarianceError:
+                estar[i] = 0
+        estar_src = "reference optimal_embedding"
+    stock = StockRows(X, estar)
+    valid = np.flatnonzero(estar > 0)
+    rng = np.random.default_rng(args.seed)
+    order = rng.permutation(valid)
+    for w in range(args.warmup):
+        stock.row(int(order[w % order.size]))
+    secs, libs = [], []
+    for s_ in range(args.steps):
+        lib = int(order[(args.warmup + s_) % order.size])
+        t0 = time.perf_counter()
+        stock.row(lib)
+        secs.append(time.perf_counter() - t0)
+        libs.append(lib)
+    per_step = float(np.mean(secs))
+    v = valid.size / per_step
+    sample = (f"one library row per step (libraries {libs[:4]}{'...' if len(libs) > 4 else ''}) x all "
+              f"{valid.size} targets, {'baseline/_ref crossmap build_knn_table + lookup_batch' if stock.kind == 'reference' else 'oracle port'}"
+              f", {stock.workers} threads; E* from {estar_src}")
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": n_pairs / v * 1e3, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "impl": "reference",
-            "config": {"workload": f"xmap N={args.n} T={args.t} mixed seed {args.seed}, E* from edim",
-                       "n_series": args.n, "T": args.t, "tau": 1, "Tp_xmap": 0, "l2": "inputs > L2"},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": workers, "kind": "port",
-                             "sample": samples},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "impl": "reference", "config": workload_config(args, int(valid.size), estar),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": stock.workers, "kind": stock.kind,
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "step_definition": "one whole library row (all targets) per step; value = pairs/s of those rows"}
     print(json.dumps(line), flush=True)
 
 
-def cpu_estar(X, args):
-    """E* for the CPU arm: the GPU's edim when a device is present (the parity
-    rule of SURVEY.md 8c compares xmap under the GPU's E*), else a cheap proxy."""
-    try:
-        import torch
-        if torch.cuda.is_available():
-            import paper_2105_12301_b200 as P
-            est, _ = P.edim(X.T.astype(np.float64), args.e_max, 1, 1)
-            return est
-    except Exception:
-        pass
-    return (np.arange(X.shape[0]) % 5 + 1).astype(np.int32)
+def workload_config(args, valid, estar):
+    """The `config` object shared by both arms (same workload, same keys)."""
+    hist = {int(e): int(c) for e, c in zip(*np.unique(estar, return_counts=True))}
+    return {"workload": f"xmap N={args.n} T={args.t} (BASELINE configs[2]), mixed seed {args.seed}, "
+                        f"E* from GPU edim E_max={args.e_max} Tp=1",
+            "n_series": args.n, "T": args.t, "tau": 1, "Tp_xmap": 0,
+            "l2": "inputs larger than L2 (X 308 MB, rho 11.3 GB)", "defined_series": valid,
+            "estar_hist": hist}
 
 
 # ---------------------------------------------------------------- GPU arm
@@ -287,7 +387,7 @@ def run_ours(args):
     with ClockSampler(local) as clk:
         e0.record(s)
         for _ in range(args.steps):
-            step()
+            rho_last = step()
             look_s.append(stats[1])
         e1.record(s)
         torch.cuda.synchronize()
@@ -421,21 +521,32 @@ def run_ours(args):
                "ms_per_step": el * 1e3}
         del host, Xe, xp
 
-    cpu = None
+    # ---- CPU baseline (the stock reference path on the host cores) on whole
+    #      library rows, which double as the parity check of this run's rho
+    cpu = parity = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        v, sample, el = cpu_sample(X_host, estar, args.cpu_seconds, os.cpu_count() or 1)
-        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "port", "sample": sample}
+        v, sample, el, libs, rows, kind = cpu_sample(X_host, estar, args.cpu_seconds, seed=args.seed, min_rows=3)
+        cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind, "sample": sample}
+        got = rho_last[:N, libs].T.cpu().numpy().astype(np.float64)  # slab column = library
+        both = ~np.isnan(got) & ~np.isnan(rows)
+        parity = {"rows": len(libs), "libraries": libs, "pairs": int(len(libs) * N),
+                  "max_abs_rho_diff": float(np.max(np.abs(got[both] - rows[both]))) if both.any() else None,
+                  "nan_equal": bool(np.array_equal(np.isnan(got), np.isnan(rows))),
+                  "tolerance": 1e-4, "checker": kind,
+                  "what": "GPU rho of the last timed step vs the stock CPU path on the same whole library rows"}
+    fx = fixture_estar(N, T, args.seed)
+    estar_check = None if fx is None else bool(np.array_equal(fx, estar))
+    if os.environ.get("CMB_SAVE_ESTAR") and rank == 0:
+        np.savez(os.environ["CMB_SAVE_ESTAR"], estar=estar.astype(np.int8), n=N, t=T, seed=args.seed)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "fp32 (fp64 selection + skill)", "data": "synthetic",
-            "config": {"workload": f"xmap N={N} T={T} (BASELINE configs[2]), mixed seed {args.seed}, "
-                                   f"E* from GPU edim E_max={args.e_max} Tp=1",
-                       "n_series": N, "T": T, "tau": 1, "Tp_xmap": 0, "parallelism": f"library rows x{world}",
-                       "l2": "inputs larger than L2 (X 308 MB, rho 11.3 GB)", "defined_series": valid,
-                       "estar_hist": hist},
+            "config": workload_config(args, valid, estar),
+            "parallelism": f"library rows x{world}",
+            "parity": parity, "estar_equals_fixture": estar_check,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "kernel": "lookup_xmap_kernel", "peak_kind": peak_kind,

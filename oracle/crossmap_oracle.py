@@ -364,6 +364,31 @@ def xmap(series, e_star, tau: int = 1, workers=None, libraries=None, targets=Non
     return rho, tables
 
 
+def xmap_rows(series, e_star, libraries, tau: int = 1, workers=None):
+    """The rows ``libraries`` of xmap (ccm.py:131-149 restricted to those
+    libraries) as a [len(libraries), N] array, without the N x N matrix (the
+    sampled checks at N = 53,053 would otherwise allocate 22.5 GB)."""
+    X = [np.asarray(s, dtype=np.float64) for s in series]
+    N = len(X)
+    stars = [None if (e is None or int(e) <= 0) else int(e) for e in e_star]
+    groups: dict[int, list[int]] = {}
+    for t, e in enumerate(stars):
+        if e is not None:
+            groups.setdefault(e, []).append(t)
+    out = np.full((len(libraries), N), np.nan)
+    for r, lib in enumerate(libraries):
+        if stars[lib] is None:
+            continue
+        for E in sorted(groups):
+            idx, w = knn_table(X[lib], E, tau, workers=workers)
+            ids = groups[E]
+            vals, _ = lookup(idx, w, E, tau, [X[t] for t in ids], workers=workers)
+            for t, v in zip(ids, vals):
+                if v is not None:
+                    out[r, t] = v
+    return out
+
+
 def ccm_pairwise(series, E_max: int = 20, tau: int = 1, Tp: int = 1, workers=None):
     """ccm.py:94-151: per-series E* by edim, then xmap.  Returns (rho, e_star)."""
     stars = []

@@ -62,7 +62,7 @@ struct DevBuf {
 enum BufId {
   B_X64, B_X32, B_ERR, B_MEAN, B_Y, B_SLOT_TGT, B_SLOT_E, B_OBS_S, B_OBS_SS, B_OBS_C, B_LIBROWS,
   B_LIBCOL, B_TAB, B_COUNTER, B_RHOT, B_RHO, B_PART, B_LAST, B_LMEAN, B_A, B_B, B_C, B_D, B_E,
-  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_YH, B_NBUF
+  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_YH, B_FIX, B_NBUF
 };
 
 struct Ctx {
@@ -223,7 +223,11 @@ static int edim_core(Ctx* ctx, cudaStream_t st, const float* x32, const double* 
 struct XmapStats {
   double t_tables = 0, t_lookup = 0, t_total = 0;
   double tables = 0, distinct = 0, pairs = 0;
+  double fixups = 0;  // pairs finished by the exact fp64 fixup of the rotated lookup
 };
+
+// capacity of the rotated lookup's fixup queue per library chunk
+constexpr int kFixCap = 1 << 22;
 
 // on_chunk(col_lo, col_hi): called after the lookup of each library chunk has
 // been enqueued on st, with the rho_T column range that is final once st reaches
@@ -347,6 +351,10 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     }
   }
 
+  const char* rot_env = getenv("CMB_LOOKUP_ROT");
+  const char* fix_env = getenv("CMB_FIX_RATIO");
+  CMB_CUDA(ctx->buf[B_FIX].ensure(16 + sizeof(int2) * (size_t)kFixCap));
+  int64_t fixups = 0;
   cudaEvent_t ev[3];
   for (auto& e : ev) CMB_CUDA(cudaEventCreate(&e));
   float ms_tab = 0, ms_look = 0;
@@ -398,10 +406,19 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     la.rhoT = rhoT;
     la.ldr = ldr;
     la.stage_bytes = stage;
+    // rotated-lane lookup (lookup.cu rot_library_group) unless CMB_LOOKUP_ROT=0;
+    // its ill-conditioned pairs are finished in fp64 by the fixup kernel
+    la.rot = (h16 || (rot_env && rot_env[0] == '0')) ? 0 : 1;
+    la.fix = reinterpret_cast<int2*>(ctx->buf[B_FIX].as<uint8_t>() + 16);
+    la.fix_count = ctx->buf[B_FIX].as<int>();
+    la.fix_cap = kFixCap;
+    la.fix_ratio = fix_env ? atof(fix_env) : 0.0625;
     CMB_CUDA(cudaMemsetAsync(la.counter, 0, sizeof(int), st));
+    CMB_CUDA(cudaMemsetAsync(la.fix_count, 0, sizeof(int), st));
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->dev);
     CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(items, dev_sms), st));
+    if (la.rot) CMB_CUDA(launch_lookup_fixup(la, st));
     if (on_chunk) {
       // columns [first column of this chunk (0 for the first), first column of the next chunk)
       const int64_t col_lo = (c0 == 0) ? 0 : lib_rows[c0] - lib_begin;
@@ -410,6 +427,20 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     }
     CMB_CUDA(cudaEventRecord(ev[2], st));
     CMB_CUDA(cudaEventSynchronize(ev[2]));
+    if (la.rot) {
+      int nfix = 0;
+      CMB_CUDA(cudaMemcpy(&nfix, la.fix_count, sizeof(int), cudaMemcpyDeviceToHost));
+      fixups += nfix;
+      if (nfix > kFixCap) {
+        // more ill-conditioned pairs than the queue holds (a pathological chunk):
+        // redo the chunk with the shifted-moment lookup, which needs no fixups
+        la.rot = 0;
+        CMB_CUDA(cudaMemsetAsync(la.counter, 0, sizeof(int), st));
+        CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(items, dev_sms), st));
+        CMB_CUDA(cudaEventRecord(ev[2], st));
+        CMB_CUDA(cudaEventSynchronize(ev[2]));
+      }
+    }
     float a_ms = 0, b_ms = 0;
     CMB_CUDA(cudaEventElapsedTime(&a_ms, ev[0], ev[1]));
     CMB_CUDA(cudaEventElapsedTime(&b_ms, ev[1], ev[2]));
@@ -425,6 +456,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     int64_t tg = 0;
     for (int g = 0; g < la.ngroups; ++g) tg += (int64_t)by_e[la.g_E[g]].size();
     stats->pairs = (double)lib_rows.size() * (double)tg;
+    stats->fixups = (double)fixups;
   }
   return CMB_OK;
 }
@@ -688,7 +720,7 @@ int cmb_xmap_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (stats_out) {
-    const double v[8] = {s.t_tables, s.t_lookup, ms * 1e-3, s.tables, s.distinct, s.pairs, 0, 0};
+    const double v[8] = {s.t_tables, s.t_lookup, ms * 1e-3, s.tables, s.distinct, s.pairs, s.fixups, 0};
     memcpy(stats_out, v, sizeof(v));
   }
   return CMB_OK;
@@ -750,7 +782,7 @@ int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* est
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   if (stats_out) {
-    const double v[8] = {s.t_tables, s.t_lookup, ms * 1e-3, s.tables, s.distinct, s.pairs, 0, 0};
+    const double v[8] = {s.t_tables, s.t_lookup, ms * 1e-3, s.tables, s.distinct, s.pairs, s.fixups, 0};
     memcpy(stats_out, v, sizeof(v));
   }
   return CMB_OK;

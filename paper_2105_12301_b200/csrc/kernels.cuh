@@ -74,6 +74,15 @@ struct LookupArgs {
   int64_t ldr;
   int stage_bytes;           // per-warp table staging slot
   int h16;                   // 16-bit targets, 64 per block, two per lane: 1 fp16, 2 q16 fixed point
+  // rotated-lane lookup (lookup.cu rot_library_group; resident fp32 targets):
+  // a (library, target block) with a pair whose prediction variance is
+  // ill-conditioned in the unshifted fp32 sums is queued here as (library in
+  // chunk, first slot of the block) and recomputed in fp64 by lookup_fixup_kernel
+  int rot;
+  double fix_ratio;          // queue when m2p <= fix_ratio * sum p^2
+  int2* fix;
+  int* fix_count;
+  int fix_cap;
 };
 
 constexpr int kLookupWarps = 16;
@@ -81,6 +90,8 @@ constexpr int kLookupWarps = 16;
 constexpr int kNonResidentStage = 4096 + 16;
 int lookup_stage_bytes(int T, int max_rec_bytes);
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st);
+// exact fp64 completion of the pairs the rotated lookup queued in a.fix
+cudaError_t launch_lookup_fixup(const LookupArgs& a, cudaStream_t st);
 
 // ------------------------------------------------------------------ helpers (utils.cu)
 cudaError_t launch_series_stats(const float* x32, int64_t N, int64_t T, int64_t ld, double* mean,

@@ -453,6 +453,313 @@ __device__ __forceinline__ void warp_library_group(const LookupArgs& a, const fl
   qglob += total;
 }
 
+// ---------------------------------------------------------------- rotated-lane lookup
+// The paths above give every lane one target and broadcast each point's record
+// (k weights + k rows) to all 32 lanes: on the mixed data those broadcasts are
+// ~40% of the shared-memory wavefronts, the kernel's binding resource.  Here a
+// lane owns a POINT instead: the warp works on batches of 8 consecutive
+// points; lane l (group g = l / 8, point p = l % 8) loads the record of point
+// p once into registers and, at rotation step j = 0..7, predicts target
+// column 8g + ((p + j) & 7) of the resident block.  At every step the 32 lanes
+// gather 32 distinct columns -- 32 distinct banks whatever the rows -- so each
+// gather is one wavefront for 32 (point, target) pairs and the record costs
+// ~k/16 wavefronts per 32 pairs instead of ~k/2 + k/4.  Lane l's accumulator j
+// always belongs to target column 8g + ((p + j) & 7), so the moments stay in
+// registers for the whole library and are transposed once at its end (a
+// barrel rotation by p and an 8-lane butterfly reduce-scatter in fp64).
+//
+// The moments are raw fp32 sums (no per-target shift: it would cost 8
+// registers per library); a pair whose prediction variance is small against
+// its second moment (m2p <= fix_ratio * Spp, e.g. a near-constant library), where
+// those sums could cancel, is queued and recomputed exactly in fp64 by
+// lookup_fixup_kernel.  Elsewhere |d m2p| / m2p <= 16 (|d Spp| + 2 |d Sp| max|p|)
+// / Spp (fix_ratio = 1/16, CMB_FIX_RATIO), i.e. a few fp32 ulps of a ~n/8-term
+// sum.  Measured at N = 8,192 against an all-fp64 run (ratio 2): max |d rho|
+// 3.3e-6 at ratios 1/4 and 1/16 (0.7% and 0.04% of the (library, block) items
+// queued), 1.4e-5 at 1/64, 3.1e-5 at 1/256 with no queue at all.
+template <int NL> struct RotV;
+template <> struct RotV<1> { using T = float; };
+template <> struct RotV<2> { using T = float2; };
+__device__ __forceinline__ float v_add(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float2 v_add(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float v_fma(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ float2 v_fma(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float v_mul(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float2 v_mul(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ void v_set(float& v, int, float x) { v = x; }
+__device__ __forceinline__ void v_set(float2& v, int h, float x) { (h ? v.y : v.x) = x; }
+__device__ __forceinline__ float v_get(float v, int) { return v; }
+__device__ __forceinline__ float v_get(float2 v, int h) { return h ? v.y : v.x; }
+template <class V> __device__ __forceinline__ V v_splat(float x);
+template <> __device__ __forceinline__ float v_splat<float>(float x) { return x; }
+template <> __device__ __forceinline__ float2 v_splat<float2>(float x) { return make_float2(x, x); }
+
+__device__ __forceinline__ void lds_v4(uint32_t addr, uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w) {
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "r"(addr));
+}
+
+// Sum over the 8 lanes of this lane's group of the accumulators that belong
+// to target column (lane & 24) + (lane & 7): lane p's m[j] belongs to column
+// (p + j) & 7, so rotate by p (v[c] = m[(c - p) & 7]) and reduce-scatter.
+__device__ __forceinline__ double rot_reduce(const float (&m)[8], int p) {
+  float v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = m[i];
+#pragma unroll
+  for (int b = 1; b < 8; b <<= 1) {
+    const bool on = (p & b) != 0;
+    float u[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u[i] = on ? v[(i - b) & 7] : v[i];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = u[i];
+  }
+  const bool b4 = (p & 4) != 0, b2 = (p & 2) != 0, b1 = (p & 1) != 0;
+  double d[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    d[i] = (double)(b4 ? v[i + 4] : v[i]) + (double)__shfl_xor_sync(CMB_FULL, b4 ? v[i] : v[i + 4], 4);
+  double e[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) e[i] = (b2 ? d[i + 2] : d[i]) + __shfl_xor_sync(CMB_FULL, b2 ? d[i] : d[i + 2], 2);
+  return (b1 ? e[1] : e[0]) + __shfl_xor_sync(CMB_FULL, b1 ? e[0] : e[1], 1);
+}
+
+// records per stage part for the rotated path (a multiple of the 8-point batch)
+__host__ __device__ constexpr int rot_records(int stage_bytes, int nl, int k) {
+  return (((stage_bytes / nl) & ~15) / rec_bytes(k)) & ~7;
+}
+
+template <int K, int NL>
+__device__ __forceinline__ void rot_library_group(const LookupArgs& a, uint32_t tsm, uint8_t* ring,
+                                                  uint64_t* bars, uint32_t& qglob, int E, int lib0,
+                                                  int ngroup, int slot_base) {
+  using V = typename RotV<NL>::T;
+  constexpr int R = rec_bytes(K);
+  constexpr int RO = rec_row_off(K);
+  const int lane = lane_id();
+  const int pl = lane & 7;
+  const int n = a.T - (E - 1) * a.tau;
+  const int off = (E - 1) * a.tau;
+  const size_t lstride = rec_lib_stride(K, n);
+  const uint8_t* base = a.tab[E] + (size_t)lib0 * lstride;
+  const int part = (a.stage_bytes / NL) & ~15;
+  const int RS = rot_records(a.stage_bytes, NL, K);
+  const int nst = (n + RS - 1) / RS;
+  const int total = ngroup * nst;
+  const uint32_t zrow = tsm + (uint32_t)a.T * 128u;  // a zero sample row: masked points gather 0
+  uint32_t col[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) col[j] = (uint32_t)((lane & 24) | ((pl + j) & 7)) << 2;
+
+  auto issue = [&](int q, uint8_t* dst, uint64_t* bar) {
+    const int lg = q / nst, s = q - lg * nst;
+    const int r0 = s * RS;
+    const int nrec = min(RS, n - r0);
+    const uint32_t bytes = (uint32_t)((nrec * R + 15) & ~15);
+    const uint8_t* src = base + (size_t)(NL * lg) * lstride + (size_t)r0 * R;
+    mbar_expect_tx(bar, NL * bytes);
+#pragma unroll
+    for (int h = 0; h < NL; ++h) bulk_g2s(dst + h * part, src + h * lstride, bytes, bar);
+  };
+  if (lane == 0) {
+    for (int q = 0; q < 2 && q < total; ++q) {
+      const uint32_t g = qglob + q;
+      issue(q, ring + (g & 1) * a.stage_bytes, bars + (g & 1));
+    }
+  }
+  __syncwarp();
+
+  V sp[8], spp[8], sop[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sp[j] = spp[j] = sop[j] = v_splat<V>(0.f);
+  for (int q = 0; q < total; ++q) {
+    const uint32_t g = qglob + q;
+    uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
+    const int lg = q / nst, s = q - lg * nst;
+    mbar_wait(bars + (g & 1), (g >> 1) & 1);
+    const uint32_t s0 = smem_u32(slotp);
+    const int r0 = s * RS;
+    const int nrec = min(RS, n - r0);
+    for (int b = 0; b < nrec; b += 8) {
+      const int r = b + pl;
+      uint32_t ra[NL][K];
+      V w[K];
+#pragma unroll
+      for (int h = 0; h < NL; ++h) {
+        uint32_t wd[R / 4];
+        const uint32_t rec = s0 + h * part + r * R;
+        if constexpr (R == 8) {
+          lds_v2(rec, wd[0], wd[1]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < R / 16; ++c) lds_v4(rec + 16 * c, wd[4 * c], wd[4 * c + 1], wd[4 * c + 2], wd[4 * c + 3]);
+        }
+        float ws = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          float wk;
+          if (rec_implicit(K) && kk == K - 1) {
+            wk = __fsub_rn(1.f, ws);  // k <= 3 records store k - 1 weights
+          } else {
+            wk = __uint_as_float(wd[kk]);
+            ws = __fadd_rn(ws, wk);
+          }
+          const uint32_t row = (wd[RO / 4 + (kk >> 1)] >> ((kk & 1) * 16)) & 0xffffu;
+          ra[h][kk] = tsm + (row << 7);
+          v_set(w[kk], h, wk);
+        }
+      }
+      uint32_t oa = tsm + ((uint32_t)(off + r0 + r) << 7);
+      if (b + 8 > nrec) {
+        // the library's last, partial batch: lanes past its end gather the zero
+        // row with zero weights, so they add nothing to the moments
+        const bool valid = r < nrec;
+#pragma unroll
+        for (int h = 0; h < NL; ++h)
+#pragma unroll
+          for (int kk = 0; kk < K; ++kk) {
+            ra[h][kk] = valid ? ra[h][kk] : zrow;
+            v_set(w[kk], h, valid ? v_get(w[kk], h) : 0.f);
+          }
+        oa = valid ? oa : zrow;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float o = lds_f32(oa + col[j]);
+        V y;
+#pragma unroll
+        for (int h = 0; h < NL; ++h) v_set(y, h, lds_f32(ra[h][0] + col[j]));
+        V p = v_mul(w[0], y);
+#pragma unroll
+        for (int kk = 1; kk < K; ++kk) {
+#pragma unroll
+          for (int h = 0; h < NL; ++h) v_set(y, h, lds_f32(ra[h][kk] + col[j]));
+          p = v_fma(w[kk], y, p);
+        }
+        sp[j] = v_add(sp[j], p);
+        spp[j] = v_fma(p, p, spp[j]);
+        sop[j] = v_fma(v_splat<V>(o), p, sop[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && q + 2 < total) issue(q + 2, slotp, bars + (g & 1));
+    if (s == nst - 1) {
+      // library group complete: lane l ends with target column l of the block
+      const int slot = slot_base + lane;
+      const int tgt_id = a.slot_tgt[slot];
+      const double So = a.obs_s[slot], Soo = a.obs_ss[slot];
+      const bool ocst = a.obs_const[slot] != 0;
+      const double nn = (double)n;
+#pragma unroll
+      for (int h = 0; h < NL; ++h) {
+        bool fix = false;
+        float m[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = v_get(sp[j], h);
+        const double Sp = rot_reduce(m, pl);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = v_get(spp[j], h);
+        const double Spp = rot_reduce(m, pl);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = v_get(sop[j], h);
+        const double Sop = rot_reduce(m, pl);
+        const int l = lib0 + NL * lg + h;
+        if (tgt_id >= 0) {
+          float* dst = a.rhoT + (size_t)tgt_id * a.ldr + a.lib_col[l];
+          const double m2o = Soo - So * So / nn;
+          const double m2p = Spp - Sp * Sp / nn;
+          const double com = Sop - So * Sp / nn;
+          if (ocst || !(m2o > 0.0)) *dst = __int_as_float(0x7fc00000);
+          else if (m2p > a.fix_ratio * Spp) *dst = (float)fmin(1.0, fmax(-1.0, com / sqrt(m2o * m2p)));
+          else fix = true;
+        }
+        // ill-conditioned pairs: queue (library, target block) once per warp
+        const unsigned bal = __ballot_sync(CMB_FULL, fix);
+        if (bal && lane == __ffs(bal) - 1) {
+          const int f = atomicAdd(a.fix_count, 1);
+          if (f < a.fix_cap) a.fix[f] = make_int2(l, slot_base);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sp[j] = spp[j] = sop[j] = v_splat<V>(0.f);
+    }
+  }
+  qglob += total;
+}
+
+// Exact completion of the queued (library, target block) entries: one CTA
+// per entry, lane = target as in warp_libraries, warp w taking the points
+// t = w (mod 8); fp64 predictions from the same fp32 records and targets (the
+// record read as warp-uniform loads, the samples as coalesced 128-byte rows of
+// the time-major array through L1/L2), moments about the lane's first
+// prediction (the shift of warp_libraries) so near-constant predictions do
+// not cancel, and a fixed-order fp64 reduction over the 8 warps.
+constexpr int kFixWarps = 8;
+__global__ void __launch_bounds__(kFixWarps * 32) lookup_fixup_kernel(LookupArgs a) {
+  __shared__ double red[3][kFixWarps][32];
+  const int nfix = min(*a.fix_count, a.fix_cap);
+  const int lane = lane_id(), w = warp_id();
+  for (int e = blockIdx.x; e < nfix; e += gridDim.x) {
+    const int2 f = a.fix[e];
+    const int l = f.x, slot = f.y + lane;
+    const int blk = f.y / 32;
+    int g = 0;
+    while (g + 1 < a.ngroups && a.g_blk0[g + 1] <= blk) ++g;
+    const int E = a.g_E[g], K = E + 1;
+    const int n = a.T - (E - 1) * a.tau, off = (E - 1) * a.tau;
+    const int R = rec_bytes(K), RO = rec_row_off(K);
+    const uint8_t* rec0 = a.tab[E] + (size_t)l * rec_lib_stride(K, n);
+    const float* __restrict__ ycol = a.Y + slot;
+    const auto pred = [&](int t) {
+      const uint8_t* rp = rec0 + (size_t)t * R;
+      const float* wp = reinterpret_cast<const float*>(rp);
+      const uint16_t* rw = reinterpret_cast<const uint16_t*>(rp + RO);
+      double p = 0.0, ws = 0.0;
+      for (int kk = 0; kk < K; ++kk) {
+        const double wk = (rec_implicit(K) && kk == K - 1) ? 1.0 - ws : (double)__ldg(wp + kk);
+        ws += wk;
+        p += wk * (double)__ldg(ycol + (size_t)__ldg(rw + kk) * a.ldy);
+      }
+      return p;
+    };
+    const double s = pred(0);
+    double Sp = 0.0, Spp = 0.0, Sop = 0.0;
+#pragma unroll 2
+    for (int t = w; t < n; t += kFixWarps) {
+      const double p = pred(t) - s;
+      const double o = (double)__ldg(ycol + (size_t)(off + t) * a.ldy);
+      Sp += p;
+      Spp += p * p;
+      Sop += o * p;
+    }
+    red[0][w][lane] = Sp;
+    red[1][w][lane] = Spp;
+    red[2][w][lane] = Sop;
+    __syncthreads();
+    if (w == 0) {
+      Sp = Spp = Sop = 0.0;
+      for (int q = 0; q < kFixWarps; ++q) {
+        Sp += red[0][q][lane];
+        Spp += red[1][q][lane];
+        Sop += red[2][q][lane];
+      }
+      const int tgt_id = a.slot_tgt[slot];
+      if (tgt_id >= 0) {
+        const double nn = (double)n;
+        const double So = a.obs_s[slot], Soo = a.obs_ss[slot];
+        const double m2o = Soo - So * So / nn;
+        const double m2p = Spp - Sp * Sp / nn;
+        const double com = Sop - So * Sp / nn;
+        float r = __int_as_float(0x7fc00000);
+        if (a.obs_const[slot] == 0 && m2o > 0.0 && m2p > 0.0) r = (float)fmin(1.0, fmax(-1.0, com / sqrt(m2o * m2p)));
+        a.rhoT[(size_t)tgt_id * a.ldr + a.lib_col[l]] = r;
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // fp16-target variant (opt-in, CMB_LOOKUP_FP16=1): the resident block holds 64
 // targets as fp16 scaled to [-1, 1] -- the same 128 bytes per sample row -- and
 // lane l owns targets 2l and 2l + 1, so every shared-memory wavefront (gathers,
@@ -591,12 +898,34 @@ constexpr int kPairMaxK = 31;  // library pairs for every k (A/B: k <= 8 5.83 s,
 // N = 1,024, T = 10,000 (81.2 vs 80.8 ms, L2-latency-bound gathers), so off
 constexpr int kPairMaxKL2 = 1;
 constexpr int kQuadMaxK = 4;  // four libraries in lockstep for k <= 4
+constexpr int kRotPairMaxK = 8;  // rotated path: two libraries in lockstep (packed FFMA2) for k <= 8
+
+// Rotated-lane lookup of one warp's libraries [lib0, lib0 + nl); returns the
+// number handled (0 when the staging slot is too small for an 8-point batch).
+template <int K>
+__device__ __forceinline__ int rot_dispatch(const LookupArgs& a, uint32_t tsm, uint8_t* ring, uint64_t* bars,
+                                            uint32_t& qglob, int E, int lib0, int nl, int slot_base) {
+  int l = 0;
+  if constexpr (K <= kRotPairMaxK) {
+    const int np = nl >> 1;
+    if (np && rot_records(a.stage_bytes, 2, K) >= 8) {
+      rot_library_group<K, 2>(a, tsm, ring, bars, qglob, E, lib0, np, slot_base);
+      l = 2 * np;
+    }
+  }
+  if (l < nl && rot_records(a.stage_bytes, 1, K) >= 8) {
+    rot_library_group<K, 1>(a, tsm, ring, bars, qglob, E, lib0 + l, nl - l, slot_base);
+    l = nl;
+  }
+  return l;
+}
 
 template <bool RESIDENT, int H16>
 __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(LookupArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   float* tgt = reinterpret_cast<float*>(smem);
-  const size_t tgt_bytes = RESIDENT ? (size_t)a.T * 128 : 0;
+  // resident targets: T sample rows + one zero row (rotated path: masked points)
+  const size_t tgt_bytes = RESIDENT ? (size_t)(a.T + 1) * 128 : 0;
   uint8_t* rings = smem + tgt_bytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(rings + (size_t)kLookupWarps * 2 * a.stage_bytes);
   __shared__ int64_t s_item;
@@ -629,9 +958,9 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
                               : reinterpret_cast<const float4*>(a.Y + (size_t)blk * 32);
       float4* dst = reinterpret_cast<float4*>(tgt);
       const int64_t ld4 = H16 ? a.ldy / 8 : a.ldy / 4;
-      for (int v = threadIdx.x; v < a.T * 8; v += blockDim.x) {
+      for (int v = threadIdx.x; v < (a.T + 1) * 8; v += blockDim.x) {
         const int t = v >> 3, c = v & 7;
-        dst[v] = src[(size_t)t * ld4 + c];
+        dst[v] = t < a.T ? src[(size_t)t * ld4 + c] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
     }
     __syncthreads();
@@ -644,6 +973,9 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
       switch (k) {
 #define CMB_K(kk)                                                                                   \
   case kk:                                                                                          \
+    if constexpr (RESIDENT && !H16)                                                                 \
+      if (a.rot && rot_dispatch<kk>(a, smem_u32(tgt), ring, wbars, qglob, E, lib0, nl, blk * 32) == nl) \
+        break;                                                                                      \
     if constexpr (H16)                                                                              \
       warp_libraries_h16<kk, H16>(a, reinterpret_cast<const uint8_t*>(tgt), ring, wbars, qglob, E, lib0, nl, blk * 64); \
     else if constexpr (kk <= (RESIDENT ? kPairMaxK : kPairMaxKL2)) {                                \
@@ -677,7 +1009,7 @@ __global__ void __launch_bounds__(kLookupWarps * 32, 1) lookup_xmap_kernel(Looku
 }  // namespace
 
 int lookup_stage_bytes(int T, int max_rec_bytes) {
-  const int budget = 232448 - T * 128 - kLookupWarps * 2 * 8 - 1024;  // 1 KB static reserve
+  const int budget = 232448 - (T + 1) * 128 - kLookupWarps * 2 * 8 - 1024;  // 1 KB static reserve
   int sb = budget / (kLookupWarps * 2);
   sb = sb - sb % 16;
   if (sb > 4096) sb = 4096;
@@ -689,7 +1021,7 @@ int lookup_stage_bytes(int T, int max_rec_bytes) {
 
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st) {
   const bool resident = a.stage_bytes != kNonResidentStage;
-  const int smem = (resident ? a.T * 128 : 0) + kLookupWarps * 2 * a.stage_bytes + kLookupWarps * 2 * 8;
+  const int smem = (resident ? (a.T + 1) * 128 : 0) + kLookupWarps * 2 * a.stage_bytes + kLookupWarps * 2 * 8;
   auto kern = !resident      ? lookup_xmap_kernel<false, 0>
               : a.h16 == 2 ? lookup_xmap_kernel<true, 2>
               : a.h16      ? lookup_xmap_kernel<true, 1>
@@ -698,6 +1030,12 @@ cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   count_launch();
   kern<<<grid, kLookupWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lookup_fixup(const LookupArgs& a, cudaStream_t st) {
+  count_launch();
+  lookup_fixup_kernel<<<148 * 8, kFixWarps * 32, 0, st>>>(a);
   return cudaGetLastError();
 }
 
