@@ -408,7 +408,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     la.stage_bytes = stage;
     // rotated-lane lookup (lookup.cu rot_library_group) unless CMB_LOOKUP_ROT=0;
     // its ill-conditioned pairs are finished in fp64 by the fixup kernel
-    la.rot = (h16 || (rot_env && rot_env[0] == '0')) ? 0 : 1;
+    la.rot = h16 ? 0 : (rot_env ? atoi(rot_env) : 2);
     la.fix = reinterpret_cast<int2*>(ctx->buf[B_FIX].as<uint8_t>() + 16);
     la.fix_count = ctx->buf[B_FIX].as<int>();
     la.fix_cap = kFixCap;

@@ -627,15 +627,30 @@ __device__ __forceinline__ void rot_library_group(const LookupArgs& a, uint32_t 
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float o = lds_f32(oa + col[j]);
-        V y;
+        V p;
+        if constexpr (NL == 1 && K >= 4) {
+          // one library: even and odd neighbours as the two halves of packed
+          // FFMA2s (half the FMA instructions; two shorter dependency chains)
+          float2 p2 = __fmul2_rn(make_float2(v_get(w[0], 0), v_get(w[1], 0)),
+                                 make_float2(lds_f32(ra[0][0] + col[j]), lds_f32(ra[0][1] + col[j])));
 #pragma unroll
-        for (int h = 0; h < NL; ++h) v_set(y, h, lds_f32(ra[h][0] + col[j]));
-        V p = v_mul(w[0], y);
+          for (int kk = 2; kk + 1 < K; kk += 2)
+            p2 = __ffma2_rn(make_float2(v_get(w[kk], 0), v_get(w[kk + 1], 0)),
+                            make_float2(lds_f32(ra[0][kk] + col[j]), lds_f32(ra[0][kk + 1] + col[j])), p2);
+          float pp = __fadd_rn(p2.x, p2.y);
+          if constexpr (K & 1) pp = __fmaf_rn(v_get(w[K - 1], 0), lds_f32(ra[0][K - 1] + col[j]), pp);
+          v_set(p, 0, pp);
+        } else {
+          V y;
 #pragma unroll
-        for (int kk = 1; kk < K; ++kk) {
+          for (int h = 0; h < NL; ++h) v_set(y, h, lds_f32(ra[h][0] + col[j]));
+          p = v_mul(w[0], y);
 #pragma unroll
-          for (int h = 0; h < NL; ++h) v_set(y, h, lds_f32(ra[h][kk] + col[j]));
-          p = v_fma(w[kk], y, p);
+          for (int kk = 1; kk < K; ++kk) {
+#pragma unroll
+            for (int h = 0; h < NL; ++h) v_set(y, h, lds_f32(ra[h][kk] + col[j]));
+            p = v_fma(w[kk], y, p);
+          }
         }
         sp[j] = v_add(sp[j], p);
         spp[j] = v_fma(p, p, spp[j]);
@@ -683,6 +698,161 @@ __device__ __forceinline__ void rot_library_group(const LookupArgs& a, uint32_t 
       }
 #pragma unroll
       for (int j = 0; j < 8; ++j) sp[j] = spp[j] = sop[j] = v_splat<V>(0.f);
+    }
+  }
+  qglob += total;
+}
+
+// Two-target variant for larger k (rot2): each half-warp runs its own
+// library of a pair; lane l (half h = l / 16, group g = (l / 8) & 1, point
+// p = l % 8) gathers a COLUMN PAIR per neighbour with one 8-byte load -- pair
+// 8g + ((p + j) & 7) at step j, so a half-warp's 16 lanes read 16 distinct
+// pairs (all 32 banks) whatever the rows.  Per 32 (point, target) pairs that is
+// the same k gather wavefronts, half the record traffic (a record serves 16
+// targets instead of 8) and about half the instructions of rot_library_group
+// (one load + address per two targets), which leaves the shared-memory pipe as
+// the only limiter for large k.  Accumulators: 8 steps x 3 moments x float2.
+__device__ __forceinline__ float2 lds_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+
+template <int K>
+__device__ __forceinline__ void rot2_library_pairs(const LookupArgs& a, uint32_t tsm, uint8_t* ring,
+                                                   uint64_t* bars, uint32_t& qglob, int E, int lib0,
+                                                   int nl, int slot_base) {
+  constexpr int R = rec_bytes(K);
+  constexpr int RO = rec_row_off(K);
+  const int lane = lane_id();
+  const int h = lane >> 4;
+  const int pl = lane & 7;
+  const uint32_t gcol = (uint32_t)(lane & 8) << 3;  // byte offset of the group's 8 column pairs
+  const int n = a.T - (E - 1) * a.tau;
+  const int off = (E - 1) * a.tau;
+  const size_t lstride = rec_lib_stride(K, n);
+  const uint8_t* base = a.tab[E] + (size_t)lib0 * lstride;
+  const int part = (a.stage_bytes / 2) & ~15;
+  const int RS = rot_records(a.stage_bytes, 2, K);
+  const int nst = (n + RS - 1) / RS;
+  const int npair = (nl + 1) >> 1;
+  const int total = npair * nst;
+  const uint32_t zrow = tsm + (uint32_t)a.T * 128u;
+
+  auto issue = [&](int q, uint8_t* dst, uint64_t* bar) {
+    const int lg = q / nst, s = q - lg * nst;
+    const int r0 = s * RS;
+    const int nrec = min(RS, n - r0);
+    const uint32_t bytes = (uint32_t)((nrec * R + 15) & ~15);
+    const int nh = (2 * lg + 1 < nl) ? 2 : 1;
+    const uint8_t* src = base + (size_t)(2 * lg) * lstride + (size_t)r0 * R;
+    mbar_expect_tx(bar, nh * bytes);
+    for (int hh = 0; hh < nh; ++hh) bulk_g2s(dst + hh * part, src + hh * lstride, bytes, bar);
+  };
+  if (lane == 0) {
+    for (int q = 0; q < 2 && q < total; ++q) {
+      const uint32_t g = qglob + q;
+      issue(q, ring + (g & 1) * a.stage_bytes, bars + (g & 1));
+    }
+  }
+  __syncwarp();
+
+  float2 sp[8], spp[8], sop[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) sp[j] = spp[j] = sop[j] = make_float2(0.f, 0.f);
+  for (int q = 0; q < total; ++q) {
+    const uint32_t g = qglob + q;
+    uint8_t* slotp = ring + (g & 1) * a.stage_bytes;
+    const int lg = q / nst, s = q - lg * nst;
+    const bool second = 2 * lg + 1 < nl;  // the pair has a second library
+    mbar_wait(bars + (g & 1), (g >> 1) & 1);
+    const uint32_t s0 = smem_u32(slotp) + ((h && second) ? part : 0);
+    const int r0 = s * RS;
+    const int nrec = min(RS, n - r0);
+    for (int b = 0; b < nrec; b += 8) {
+      const int r = b + pl;
+      uint32_t ra[K];
+      float w[K];
+      {
+        uint32_t wd[R / 4];
+        const uint32_t rec = s0 + r * R;
+#pragma unroll
+        for (int c = 0; c < R / 16; ++c) lds_v4(rec + 16 * c, wd[4 * c], wd[4 * c + 1], wd[4 * c + 2], wd[4 * c + 3]);
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          w[kk] = __uint_as_float(wd[kk]);
+          const uint32_t row = (wd[RO / 4 + (kk >> 1)] >> ((kk & 1) * 16)) & 0xffffu;
+          ra[kk] = tsm + (row << 7);
+        }
+      }
+      uint32_t oa = tsm + ((uint32_t)(off + r0 + r) << 7);
+      if (b + 8 > nrec) {
+        const bool valid = r < nrec;
+#pragma unroll
+        for (int kk = 0; kk < K; ++kk) {
+          ra[kk] = valid ? ra[kk] : zrow;
+          w[kk] = valid ? w[kk] : 0.f;
+        }
+        oa = valid ? oa : zrow;
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t c = gcol | ((uint32_t)((pl + j) & 7) << 3);
+        const float2 o = lds_f2(oa + c);
+        float2 y = lds_f2(ra[0] + c);
+        float2 p = make_float2(__fmul_rn(w[0], y.x), __fmul_rn(w[0], y.y));
+#pragma unroll
+        for (int kk = 1; kk < K; ++kk) {
+          y = lds_f2(ra[kk] + c);
+          p.x = __fmaf_rn(w[kk], y.x, p.x);
+          p.y = __fmaf_rn(w[kk], y.y, p.y);
+        }
+        sp[j] = __fadd2_rn(sp[j], p);
+        spp[j] = __ffma2_rn(p, p, spp[j]);
+        sop[j] = __ffma2_rn(o, p, sop[j]);
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && q + 2 < total) issue(q + 2, slotp, bars + (g & 1));
+    if (s == nst - 1) {
+      // pair complete: lane (h, g, p) holds column pair 8g + p of library 2 lg + h
+      const int l = lib0 + 2 * lg + h;
+      const bool live = h == 0 || second;
+      const double nn = (double)n;
+      bool fix = false;
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        float m[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = c2 ? sp[j].y : sp[j].x;
+        const double Sp = rot_reduce(m, pl);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = c2 ? spp[j].y : spp[j].x;
+        const double Spp = rot_reduce(m, pl);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) m[j] = c2 ? sop[j].y : sop[j].x;
+        const double Sop = rot_reduce(m, pl);
+        const int slot = slot_base + 2 * ((lane & 8) | pl) + c2;
+        const int tgt_id = a.slot_tgt[slot];
+        if (live && tgt_id >= 0) {
+          const double So = a.obs_s[slot], Soo = a.obs_ss[slot];
+          float* dst = a.rhoT + (size_t)tgt_id * a.ldr + a.lib_col[l];
+          const double m2o = Soo - So * So / nn;
+          const double m2p = Spp - Sp * Sp / nn;
+          const double com = Sop - So * Sp / nn;
+          if (a.obs_const[slot] != 0 || !(m2o > 0.0)) *dst = __int_as_float(0x7fc00000);
+          else if (m2p > a.fix_ratio * Spp) *dst = (float)fmin(1.0, fmax(-1.0, com / sqrt(m2o * m2p)));
+          else fix = true;
+        }
+      }
+      // ill-conditioned pairs: queue (library, target block) once per half-warp
+      const unsigned bal = __ballot_sync(CMB_FULL, fix) & (0xffffu << (16 * h));
+      if (bal && lane == __ffs(bal) - 1) {
+        const int f = atomicAdd(a.fix_count, 1);
+        if (f < a.fix_cap) a.fix[f] = make_int2(l, slot_base);
+      }
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sp[j] = spp[j] = sop[j] = make_float2(0.f, 0.f);
     }
   }
   qglob += total;
@@ -899,6 +1069,8 @@ constexpr int kPairMaxK = 31;  // library pairs for every k (A/B: k <= 8 5.83 s,
 constexpr int kPairMaxKL2 = 1;
 constexpr int kQuadMaxK = 4;  // four libraries in lockstep for k <= 4
 constexpr int kRotPairMaxK = 8;  // rotated path: two libraries in lockstep (packed FFMA2) for k <= 8
+constexpr int kRot2MinK = 9;     // two-target rotated path (rot2_library_pairs) for 9 <= k <= 24
+constexpr int kRot2MaxK = 24;
 
 // Rotated-lane lookup of one warp's libraries [lib0, lib0 + nl); returns the
 // number handled (0 when the staging slot is too small for an 8-point batch).
@@ -906,6 +1078,12 @@ template <int K>
 __device__ __forceinline__ int rot_dispatch(const LookupArgs& a, uint32_t tsm, uint8_t* ring, uint64_t* bars,
                                             uint32_t& qglob, int E, int lib0, int nl, int slot_base) {
   int l = 0;
+  if constexpr (K >= kRot2MinK && K <= kRot2MaxK) {
+    if (a.rot == 2 && rot_records(a.stage_bytes, 2, K) >= 8) {
+      rot2_library_pairs<K>(a, tsm, ring, bars, qglob, E, lib0, nl, slot_base);
+      return nl;
+    }
+  }
   if constexpr (K <= kRotPairMaxK) {
     const int np = nl >> 1;
     if (np && rot_records(a.stage_bytes, 2, K) >= 8) {
