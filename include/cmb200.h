@@ -96,9 +96,18 @@ int cmb_edim(int dev, const double* X, int64_t N, int64_t len, int E_max, int ta
  * the target's E (estar[tgt]); Tp = 0 lookup; estar[i] == 0 marks series i
  * undefined (its row and column are NaN).  X[N][len] float32 samples.
  * stats_out (nullable, 8 doubles): seconds {tables, lookup, total},
- * tables_built, distinct_E, pairs, 0, 0.                                    */
+ * tables_built, distinct_E, pairs, fixup items (library, target block pairs
+ * recomputed in fp64 by the lookup), 0.                                     */
 int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* estar, int tau,
              float* rho_out, int layout, double* stats_out);
+
+/* cmb_xmap for float64 series X[N][len] (the reference's own dtype, series.py:25):
+ * staged in float64 on the device; the fp32 sweep runs on the series minus
+ * their fp64 means (so large offsets keep their digits), kNN certification is
+ * bounded against the float64 values and uncertified rows are re-selected
+ * exactly in float64 (weights then from the float64 distances).            */
+int cmb_xmap64(int dev, const double* X, int64_t N, int64_t len, const int32_t* estar, int tau,
+               float* rho_out, int layout, double* stats_out);
 
 /* Device-resident shard of cmb_xmap for the multi-GPU driver: X_dev[N][ld]
  * (float32, on `dev`), libraries [lib_begin, lib_end); writes

@@ -20,7 +20,7 @@ from .errors import (CrossmapError, CsvFormatError, DeviceError, ParameterError,
 from .pairwise import (LAYOUT_LIB_MAJOR, LAYOUT_TGT_MAJOR, CcmConfig, CcmStats, SkillMatrix,
                        ccm_pairwise, group_by_optimal_e, xmap)
 from .skill import (OptimalEmbedding, PearsonAggregate, PredictionOutput, lookup_batch,
-                    optimal_embedding, pearson_stream, simplex_self_predict, skill_curves)
+                    near_ties, optimal_embedding, pearson_stream, simplex_self_predict, skill_curves)
 from .synthetic import coupled_logistic, gen_synthetic, logistic_map, mixed_dataset, uniform_noise
 from .tables import (DistanceMatrix, NeighborTable, build_knn_table, normalize_to_weights,
                      oracle_knn, pairwise_distances, partial_sort_topk)
@@ -39,7 +39,8 @@ def edim(values, E_max: int = DEFAULT_E_MAX, tau: int = 1, Tp: int = 1):
     1-D input -> ``EmbeddingSearch(e_star, skill_by_dim)`` (binding layout).
     2-D (time, series) input -> ``(e_star int32[N], rho float64[N, E_max])``
     computed in one batched device sweep; e_star 0 / NaN rho mark series whose
-    skill is undefined (constant series).
+    skill is undefined (constant series).  ``near_ties(rho, e_star)`` lists the
+    series whose best and runner-up skills differ by less than 1e-4.
     """
     arr = np.asarray(values, dtype=np.float64)
     if arr.ndim == 1:
@@ -67,7 +68,7 @@ __all__ = [
     "ZeroVarianceError", "as_values", "build_knn_table", "ccm", "ccm_matrix", "ccm_pairwise", "ccm_sweep",
     "coupled_logistic", "edim", "embedded_point", "gen_synthetic", "group_by_optimal_e",
     "logistic_map", "lookup_batch", "mixed_dataset", "normalize_to_weights", "optimal_embedding",
-    "oracle_knn", "pairwise_distances", "partial_sort_topk", "pearson_stream", "simplex",
+    "near_ties", "oracle_knn", "pairwise_distances", "partial_sort_topk", "pearson_stream", "simplex",
     "simplex_self_predict", "skill_curves", "uniform_noise", "valid_count", "xmap",
     "load_csv", "read_skill_matrix", "read_skill_matrix_npz", "write_skill_matrix",
     "write_skill_matrix_device", "write_skill_matrix_npz", "BenchRow", "run_bench",

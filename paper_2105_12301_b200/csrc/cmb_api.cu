@@ -65,12 +65,46 @@ enum BufId {
   B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_YH, B_FIX, B_NBUF
 };
 
+// page-locked host buffer (the pageable-output bounce slabs of xmap_host)
+struct HostBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t bytes) {
+    if (bytes <= cap) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+    if (e == cudaSuccess) cap = bytes;
+    return e;
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+// events destroyed on every exit path (early returns leaked them)
+struct EventSet {
+  std::vector<cudaEvent_t> v;
+  cudaError_t make(cudaEvent_t* e, unsigned flags) {
+    cudaError_t r = cudaEventCreateWithFlags(e, flags);
+    if (r == cudaSuccess) v.push_back(*e);
+    return r;
+  }
+  ~EventSet() {
+    for (auto e : v) cudaEventDestroy(e);
+  }
+};
+
 struct Ctx {
   int dev = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // D2H overlap of the host-buffer cross map
   std::mutex mu;
   DevBuf buf[B_NBUF];
+  HostBuf bounce[2];
   bool ready = false;
 };
 
@@ -234,9 +268,13 @@ constexpr int kFixCap = 1 << 22;
 // that point (the host-buffer entry point overlaps its D2H copy with later chunks)
 using ChunkFn = std::function<int(int64_t, int64_t)>;
 
+// X: float32 samples [N][ld] on the device.  x64_in (nullable): the caller's
+// float64 series [N][ld] when X was derived from them (cmb_xmap64: X centred,
+// err_in = per-series certification perturbation); otherwise X is promoted.
 static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64_t T, int64_t ld,
                      const int32_t* estar, int tau, int64_t lib_begin, int64_t lib_end, float* rhoT,
-                     int64_t ldr, XmapStats* stats, const ChunkFn& on_chunk = nullptr) {
+                     int64_t ldr, XmapStats* stats, const ChunkFn& on_chunk = nullptr,
+                     const double* x64_in = nullptr, const float* err_in = nullptr) {
   CMB_PARAM(tau >= 1, "tau must be >= 1, got %d", tau);
   CMB_PARAM(lib_begin >= 0 && lib_begin <= lib_end && lib_end <= N, "bad library range [%lld, %lld)",
             (long long)lib_begin, (long long)lib_end);
@@ -301,7 +339,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   CMB_CUDA(ctx->buf[B_OBS_C].ensure(slots));
   CMB_CUDA(ctx->buf[B_Y].ensure(sizeof(float) * T * ldy));
   CMB_CUDA(ctx->buf[B_MEAN].ensure(8 * N));
-  CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * ld));
+  if (!x64_in) CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * ld));
   CMB_CUDA(ctx->buf[B_LIBROWS].ensure(4 * lib_rows.size()));
   CMB_CUDA(ctx->buf[B_LIBCOL].ensure(8 * lib_col.size()));
   CMB_CUDA(ctx->buf[B_COUNTER].ensure(16));
@@ -327,7 +365,11 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
                                 slots, ctx->buf[B_OBS_S].as<double>(), ctx->buf[B_OBS_SS].as<double>(),
                                 ctx->buf[B_OBS_C].as<uint8_t>(), st));
   }
-  CMB_CUDA(launch_promote(X, N, T, ld, ctx->buf[B_X64].as<double>(), st));
+  const double* x64 = x64_in;
+  if (!x64) {
+    CMB_CUDA(launch_promote(X, N, T, ld, ctx->buf[B_X64].as<double>(), st));
+    x64 = ctx->buf[B_X64].as<double>();
+  }
 
   // ---- library chunks: tables for every needed E, then the lookup
   size_t per_lib = 0;
@@ -355,8 +397,9 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   const char* fix_env = getenv("CMB_FIX_RATIO");
   CMB_CUDA(ctx->buf[B_FIX].ensure(16 + sizeof(int2) * (size_t)kFixCap));
   int64_t fixups = 0;
+  EventSet evs;
   cudaEvent_t ev[3];
-  for (auto& e : ev) CMB_CUDA(cudaEventCreate(&e));
+  for (auto& e : ev) CMB_CUDA(evs.make(&e, 0));
   float ms_tab = 0, ms_look = 0;
   const int rpb = 128;
   for (int64_t c0 = 0; c0 < (int64_t)lib_rows.size(); c0 += C) {
@@ -364,8 +407,9 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     KnnArgs a;
     memset(&a, 0, sizeof(a));
     a.x32 = X;
-    a.x64 = ctx->buf[B_X64].as<double>();
+    a.x64 = x64;
     a.ld = ld;
+    a.err_m = err_in;
     a.lib_rows = ctx->buf[B_LIBROWS].as<int32_t>() + c0;
     a.nlib = (int)nc;
     a.L = (int)T;
@@ -447,7 +491,6 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     ms_tab += a_ms;
     ms_look += b_ms;
   }
-  for (auto& e : ev) cudaEventDestroy(e);
   if (stats) {
     stats->t_tables = ms_tab * 1e-3;
     stats->t_lookup = ms_look * 1e-3;
@@ -496,6 +539,7 @@ int cmb_shutdown(void) {
     std::lock_guard<std::mutex> l(c->mu);
     cudaSetDevice(c->dev);
     for (auto& b : c->buf) b.release();
+    for (auto& b : c->bounce) b.release();
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     c->stream = nullptr;
@@ -726,50 +770,98 @@ int cmb_xmap_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld
   return CMB_OK;
 }
 
-int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* estar, int tau,
-             float* rho_out, int layout, double* stats_out) {
-  CMB_PARAM(layout == CMB_LAYOUT_LIB_MAJOR || layout == CMB_LAYOUT_TGT_MAJOR, "bad layout %d", layout);
-  CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
-  CMB_CTX(dev);
+}  // extern "C"
+
+namespace cmb {
+
+// Host-buffer cross map behind cmb_xmap / cmb_xmap64.  Target-major output is
+// copied back per library chunk on a second stream while later chunks compute:
+// straight into rho_out when it is page-locked, else through two pinned
+// bounce slabs (a device-to-pageable copy would block the host and serialise
+// the chunks).
+static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t N, int64_t len,
+                     const int32_t* estar, int tau, float* rho_out, int layout, double* stats_out) {
   const int64_t ldr = (N + 3) / 4 * 4;
   CMB_CUDA(ctx->buf[B_X32].ensure(sizeof(float) * N * len + 256));
   CMB_CUDA(ctx->buf[B_RHOT].ensure(sizeof(float) * N * ldr));
+  EventSet evs;
   cudaEvent_t e0, e1;
-  CMB_CUDA(cudaEventCreate(&e0));
-  CMB_CUDA(cudaEventCreate(&e1));
+  CMB_CUDA(evs.make(&e0, 0));
+  CMB_CUDA(evs.make(&e1, 0));
   CMB_CUDA(cudaEventRecord(e0, st));
-  CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X32].p, X, sizeof(float) * N * len, cudaMemcpyHostToDevice, st));
+  const double* x64 = nullptr;
+  const float* err = nullptr;
+  if (f64) {
+    CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * len));
+    CMB_CUDA(ctx->buf[B_ERR].ensure(sizeof(float) * N));
+    CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X64].p, X, sizeof(double) * N * len, cudaMemcpyHostToDevice, st));
+    CMB_CUDA(launch_demote_center(ctx->buf[B_X64].as<double>(), N, len, ctx->buf[B_X32].as<float>(),
+                                  ctx->buf[B_ERR].as<float>(), st));
+    x64 = ctx->buf[B_X64].as<double>();
+    err = ctx->buf[B_ERR].as<float>();
+  } else {
+    CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X32].p, X, sizeof(float) * N * len, cudaMemcpyHostToDevice, st));
+  }
   XmapStats s;
   if (layout == CMB_LAYOUT_TGT_MAJOR) {
-    // target-major output: copy each chunk's finished columns to the host on a
-    // second stream while the next chunks compute
     if (!ctx->copy_stream) CMB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-    std::vector<cudaEvent_t> done;
+    cudaPointerAttributes attr;
+    const bool pinned = cudaPointerGetAttributes(&attr, rho_out) == cudaSuccess &&
+                        attr.type != cudaMemoryTypeUnregistered;
+    cudaGetLastError();
     const float* rt = ctx->buf[B_RHOT].as<float>();
+    // pageable output: chunk slabs go device -> pinned bounce (async) -> rho_out
+    // (host memcpy of chunk c while chunk c + 1 computes)
+    struct Pending { int64_t lo = 0, hi = 0; float* slab = nullptr; cudaEvent_t ev = nullptr; };
+    Pending pend;
+    int slot = 0;
+    auto drain = [&]() -> int {
+      if (!pend.slab) return CMB_OK;
+      CMB_CUDA(cudaEventSynchronize(pend.ev));
+      const int64_t w = pend.hi - pend.lo;
+      for (int64_t r = 0; r < N; ++r) memcpy(rho_out + r * N + pend.lo, pend.slab + r * w, sizeof(float) * w);
+      pend.slab = nullptr;
+      return CMB_OK;
+    };
     auto on_chunk = [&](int64_t lo, int64_t hi) -> int {
       if (hi <= lo) return CMB_OK;
       cudaEvent_t ev;
-      CMB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-      done.push_back(ev);
+      CMB_CUDA(evs.make(&ev, cudaEventDisableTiming));
       CMB_CUDA(cudaEventRecord(ev, st));
       CMB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev, 0));
-      CMB_CUDA(cudaMemcpy2DAsync(rho_out + lo, sizeof(float) * N, rt + lo, sizeof(float) * ldr,
+      if (pinned) {
+        CMB_CUDA(cudaMemcpy2DAsync(rho_out + lo, sizeof(float) * N, rt + lo, sizeof(float) * ldr,
+                                   sizeof(float) * (hi - lo), N, cudaMemcpyDeviceToHost, ctx->copy_stream));
+        return CMB_OK;
+      }
+      CMB_TRY(drain());  // the previous chunk's slab (its copy was queued one chunk ago)
+      const size_t need = sizeof(float) * (size_t)N * (size_t)(hi - lo);
+      CMB_CUDA(ctx->bounce[slot].ensure(need));
+      float* slab = reinterpret_cast<float*>(ctx->bounce[slot].p);
+      CMB_CUDA(cudaMemcpy2DAsync(slab, sizeof(float) * (hi - lo), rt + lo, sizeof(float) * ldr,
                                  sizeof(float) * (hi - lo), N, cudaMemcpyDeviceToHost, ctx->copy_stream));
+      cudaEvent_t cev;
+      CMB_CUDA(evs.make(&cev, cudaEventDisableTiming));
+      CMB_CUDA(cudaEventRecord(cev, ctx->copy_stream));
+      pend.lo = lo;
+      pend.hi = hi;
+      pend.slab = slab;
+      pend.ev = cev;
+      slot ^= 1;
       return CMB_OK;
     };
     const int rc = xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
-                             ctx->buf[B_RHOT].as<float>(), ldr, &s, on_chunk);
+                             ctx->buf[B_RHOT].as<float>(), ldr, &s, on_chunk, x64, err);
     cudaEvent_t copied;
-    CMB_CUDA(cudaEventCreateWithFlags(&copied, cudaEventDisableTiming));
+    CMB_CUDA(evs.make(&copied, cudaEventDisableTiming));
     CMB_CUDA(cudaEventRecord(copied, ctx->copy_stream));
     CMB_CUDA(cudaStreamWaitEvent(st, copied, 0));
     CMB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
-    cudaEventDestroy(copied);
-    for (auto ev : done) cudaEventDestroy(ev);
     if (rc) return rc;
+    CMB_TRY(drain());
   } else {
     CMB_TRY(xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
-                      ctx->buf[B_RHOT].as<float>(), ldr, &s));
+                      ctx->buf[B_RHOT].as<float>(), ldr, &s, nullptr, x64, err));
     CMB_CUDA(ctx->buf[B_RHO].ensure(sizeof(float) * N * ldr));
     CMB_CUDA(launch_transpose_f32(ctx->buf[B_RHOT].as<float>(), N, N, ldr, ctx->buf[B_RHO].as<float>(), ldr, st));
     CMB_CUDA(cudaMemcpy2DAsync(rho_out, sizeof(float) * N, ctx->buf[B_RHO].p, sizeof(float) * ldr,
@@ -779,13 +871,31 @@ int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* est
   CMB_CUDA(cudaEventSynchronize(e1));
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
   if (stats_out) {
     const double v[8] = {s.t_tables, s.t_lookup, ms * 1e-3, s.tables, s.distinct, s.pairs, s.fixups, 0};
     memcpy(stats_out, v, sizeof(v));
   }
   return CMB_OK;
+}
+
+}  // namespace cmb
+
+extern "C" {
+
+int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* estar, int tau,
+             float* rho_out, int layout, double* stats_out) {
+  CMB_PARAM(layout == CMB_LAYOUT_LIB_MAJOR || layout == CMB_LAYOUT_TGT_MAJOR, "bad layout %d", layout);
+  CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
+  CMB_CTX(dev);
+  return xmap_host(ctx, st, X, false, N, len, estar, tau, rho_out, layout, stats_out);
+}
+
+int cmb_xmap64(int dev, const double* X, int64_t N, int64_t len, const int32_t* estar, int tau,
+               float* rho_out, int layout, double* stats_out) {
+  CMB_PARAM(layout == CMB_LAYOUT_LIB_MAJOR || layout == CMB_LAYOUT_TGT_MAJOR, "bad layout %d", layout);
+  CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
+  CMB_CTX(dev);
+  return xmap_host(ctx, st, X, true, N, len, estar, tau, rho_out, layout, stats_out);
 }
 
 int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E, int tau,

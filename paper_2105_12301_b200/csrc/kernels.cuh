@@ -24,7 +24,7 @@ struct KnnArgs {
   int k_raw;                // KNN_RAW: neighbour count (else E + 1)
   int rows_per_block;
   int nrb;                  // row blocks per library
-  const float* err_m;       // per library slot: max |x32 - x64| (nullable = 0)
+  const float* err_m;       // per series row: max |x32 - x64| (nullable = 0)
   // KNN_TABLE: per E base pointer of [nlib][n_E][rec_bytes(E+1)]
   uint8_t* tab[CMB_SWEEP_MAX_E + 1];
   // KNN_EDIM
@@ -100,6 +100,8 @@ cudaError_t launch_promote(const float* x32, int64_t N, int64_t T, int64_t ld, d
                            cudaStream_t st);
 cudaError_t launch_demote(const double* x64, int64_t N, int64_t T, float* x32, float* err_m,
                           cudaStream_t st);
+cudaError_t launch_demote_center(const double* x64, int64_t N, int64_t T, float* x32, float* err_m,
+                                 cudaStream_t st);
 cudaError_t launch_build_targets(const float* x32, int64_t ld, const double* mean,
                                  const int32_t* slot_tgt, int64_t slots, int T, float* Y,
                                  int64_t ldy, cudaStream_t st);

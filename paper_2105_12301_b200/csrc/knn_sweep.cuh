@@ -74,6 +74,21 @@ __device__ __forceinline__ double sweep_err_bound(double t, int E, double M) {
   return 1.001 * (gam * (t + e1) + e1) + 1e-15 * t;
 }
 
+// A nonzero fp32 sample below 2^-50 can make the squared difference of two
+// distinct samples underflow to zero (or lose the relative error model of
+// sweep_err_bound), so such a library never takes the fp32 certification:
+// library_err returns NaN for it and every row goes through the fp64 path
+// (exact re-sort, or exact_row_select).  ADVICE r01.
+__device__ __forceinline__ bool tiny_sample(float v) { return v != 0.f && fabsf(v) < 8.881784197001252e-16f; }
+
+// Certification perturbation M of a library: max |x32 - x64| of its series
+// (err_m, indexed by series row; 0 for float32 inputs), NaN when tiny.
+template <class A>
+__device__ __forceinline__ double library_err(const A& a, int64_t srow, bool tiny) {
+  if (tiny) return __longlong_as_double(0x7ff8000000000000ll);
+  return a.err_m ? (double)a.err_m[srow] : 0.0;
+}
+
 template <int E_HI>
 __device__ __forceinline__ double exact_sqdist_u(const double* x, int i, int j, int E, int tau) {
   double acc = 0.0;
@@ -429,10 +444,21 @@ static __device__ __noinline__ unsigned lane_finish(const KnnArgs* __restrict__ 
         const int k = k_of(a.mode, a.k_raw, e);
         const float dk1 = Le[k - 1].d;
         const float dk = Le[min(k, Kp - 1)].d;
-        bool ok = (Kp == nE - 1) || (M == 0.0 && dk == 0.f);
+        bool ok = !isnan(M) && ((Kp == nE - 1) || (M == 0.0 && dk == 0.f));
         if (!ok && isfinite(dk) && dk > 1e-30f) {
           const double A = dk1, B = dk;
           ok = A + sweep_err_bound(A, E, M) < B - sweep_err_bound(B, E, M);
+        }
+        if (ok && M != 0.0) {
+          // float64 inputs (M > 0): the weights exp(-d_q / d_scale) are as
+          // sensitive as the smallest listed distance, so every fp32 distance
+          // must be known to 1e-5 relative -- an fp32 zero could be a tiny
+          // positive fp64 distance that the reference uses as its scale.  (With
+          // M = 0 the bound is < 2e-6 relative and zeros are exact.)
+          for (int q = 0; q < k && ok; ++q) {
+            const float dq = Le[q].d;
+            ok = dq > 0.f && sweep_err_bound(dq, E, M) <= 1e-5 * (double)dq;
+          }
         }
         if (ok) {
           // scale: the smallest distance, or the first positive one (knn.py:194-199)
@@ -590,7 +616,13 @@ knn_sweep_kernel(const __grid_constant__ KnnArgs a) {
 
   // stage the library series (plus zero padding for out-of-range candidates)
   const int span = L + E_HI * tau + kStep + 32;
-  for (int t = threadIdx.x; t < span; t += kThreads) xs[t] = (t < L) ? gx[t] : 0.f;
+  bool tiny = false;
+  for (int t = threadIdx.x; t < span; t += kThreads) {
+    const float v = (t < L) ? gx[t] : 0.f;
+    xs[t] = v;
+    tiny |= tiny_sample(v);
+  }
+  tiny = __syncthreads_or(tiny);
   if (a.x64_smem)
     for (int t = threadIdx.x; t < Tfull; t += kThreads) x64s[t] = gx64[t];
   const double* __restrict__ xp = a.x64_smem ? x64s : gx64;
@@ -621,7 +653,7 @@ knn_sweep_kernel(const __grid_constant__ KnnArgs a) {
   }
   __syncthreads();
 
-  const double M = a.err_m ? (double)a.err_m[lib] : 0.0;
+  const double M = library_err(a, srow, tiny);
   const int e_hi = a.e_hi;
   const int rpw = (a.rows_per_block + kWarps - 1) / kWarps;
   const int r0 = rb * a.rows_per_block + w * rpw;

@@ -256,12 +256,15 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
 
   // stage the library series as (x[p], x[p + kHalf]) pairs, +inf past the end
   const int zspan = L + kHalf + 32 + EHR;
+  bool tiny = false;
   for (int q = threadIdx.x; q < zspan; q += kThreads) {
     float2 v;
     v.x = (q < L) ? gx[q] : kInfF;
     v.y = (q + kHalf < L) ? gx[q + kHalf] : kInfF;
     Z[zi(q)] = v;
+    tiny |= tiny_sample(v.x);
   }
+  tiny = __syncthreads_or(tiny);
   if (a.x64_smem)
     for (int t = threadIdx.x; t < Tfull; t += kThreads) x64s[t] = gx64[t];
   const double* __restrict__ xp = a.x64_smem ? x64s : gx64;
@@ -291,7 +294,7 @@ knn_tile_kernel(const __grid_constant__ KnnArgs a) {
   }
   __syncthreads();
 
-  const double M = a.err_m ? (double)a.err_m[lib] : 0.0;
+  const double M = library_err(a, srow, tiny);
   const int e_hi = a.e_hi;
   // rows interleaved over the warps (no state carries between rows), so the
   // last, partial block of a library keeps all eight warps busy

@@ -56,6 +56,55 @@ __global__ void demote_kernel(const double* __restrict__ x, int64_t N, int64_t T
   }
 }
 
+// float64 series -> float32 samples about the series mean (the cross map's
+// float64 entry): x32 = fl32(x64 - mean64), so large offsets do not eat the
+// fp32 mantissa; err = max |x32 - (x64 - mean64)| (+ the fp64 rounding of the
+// subtraction), the perturbation M the kNN certification bounds.  Distances
+// are translation invariant; the exact fp64 paths use the uncentred x64.
+__global__ void demote_center_kernel(const double* __restrict__ x, int64_t T, float* __restrict__ y,
+                                     float* __restrict__ err) {
+  const int64_t s = blockIdx.x;
+  __shared__ double wsum[32];
+  __shared__ float wm[32];
+  __shared__ double s_mean;
+  double acc = 0.0;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) acc += x[s * T + t];
+  acc = warp_sum_d(acc);
+  if (lane_id() == 0) wsum[warp_id()] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += wsum[q];
+    s_mean = tot / (double)T;
+  }
+  __syncthreads();
+  const double mu = s_mean;
+  float m = 0.f;
+  double amax = 0.0;
+  for (int64_t t = threadIdx.x; t < T; t += blockDim.x) {
+    const double v = x[s * T + t];
+    const double c = v - mu;
+    const float f = (float)c;
+    y[s * T + t] = f;
+    m = fmaxf(m, (float)fabs((double)f - c) * 1.0000001f);
+    amax = fmax(amax, fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    m = fmaxf(m, __shfl_xor_sync(CMB_FULL, m, o));
+    amax = fmax(amax, __shfl_xor_sync(CMB_FULL, amax, o));
+  }
+  if (lane_id() == 0) { wm[warp_id()] = m; wsum[warp_id()] = amax; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r = 0.f;
+    double a = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) { r = fmaxf(r, wm[q]); a = fmax(a, wsum[q]); }
+    // |fl(v - mu) - (v - mu)| <= 2^-53 (|v| + |mu|)
+    err[s] = r + (float)(2.3e-16 * (a + fabs(mu)));
+  }
+}
+
 // Y[t][slot] = x[tgt(slot)][t] - mean(tgt)   (32 x 32 shared-memory transpose)
 __global__ void build_targets_kernel(const float* __restrict__ x, int64_t ld,
                                      const double* __restrict__ mean,
@@ -375,6 +424,14 @@ cudaError_t launch_demote(const double* x64, int64_t N, int64_t T, float* x32, f
   if (N == 0) return cudaSuccess;
   count_launch();
   demote_kernel<<<(unsigned)N, 256, 0, st>>>(x64, N, T, x32, err_m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_demote_center(const double* x64, int64_t N, int64_t T, float* x32, float* err_m,
+                                 cudaStream_t st) {
+  if (N == 0) return cudaSuccess;
+  count_launch();
+  demote_center_kernel<<<(unsigned)N, 256, 0, st>>>(x64, T, x32, err_m);
   return cudaGetLastError();
 }
 

@@ -115,16 +115,21 @@ def xmap(values, e_star, tau: int = 1, layout: int = LAYOUT_LIB_MAJOR, dtype=np.
         raise ParameterError(f"{est.size} dimensions for {N} series")
     if tau < 1:
         raise ParameterError(f"tau must be >= 1, got {tau}")
-    Xs = np.ascontiguousarray(X.T, dtype=np.float32)  # series-major samples
+    # float32 input runs the float32 entry; anything else is staged in float64
+    # (the reference's dtype, series.py:25): cmb_xmap64 centres each series in
+    # fp64 before the fp32 sweep and certifies neighbours against the fp64 values
+    f32 = X.dtype == np.float32
+    Xs = np.ascontiguousarray(X.T, dtype=np.float32 if f32 else np.float64)  # series-major samples
     # beyond the fused kernels' formats (E* > NATIVE_E_MAX, or T past the 16-bit
     # row indices of the table records) the affected pairs take the reference's
     # composition on the device: build_knn_table + lookup_batch per (library, E)
     wide = (est > NATIVE_E_MAX) | ((T > NATIVE_T_MAX) & (est > 0))
     if wide.any():
-        return _xmap_with_wide(Xs, est, wide, tau, layout, dtype, stats)
+        return _xmap_with_wide(np.ascontiguousarray(Xs, dtype=np.float32), est, wide, tau, layout, dtype, stats)
     out = np.empty((N, N), dtype=np.float32)
     st = np.zeros(8)
-    nat.call("cmb_xmap", nat.device(), nat.ptr(Xs), N, T, nat.ptr(est), tau, nat.ptr(out), layout, nat.ptr(st))
+    nat.call("cmb_xmap" if f32 else "cmb_xmap64", nat.device(), nat.ptr(Xs), N, T, nat.ptr(est), tau,
+             nat.ptr(out), layout, nat.ptr(st))
     if stats is not None:
         stats.update(seconds_table_build=float(st[0]), seconds_lookup=float(st[1]),
                      seconds_total=float(st[2]), tables_built=int(st[3]), distinct_e=int(st[4]),

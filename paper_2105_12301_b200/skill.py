@@ -186,6 +186,25 @@ def skill_curves(X: np.ndarray, e_max: int, tau: int, tp: int) -> tuple[np.ndarr
     return rho, est
 
 
+def near_ties(rho: np.ndarray, est: np.ndarray, tol: float = 1e-4) -> list[dict]:
+    """Series whose E* is fragile: the best curve value and the runner-up differ
+    by less than ``tol`` (SURVEY.md 8c parity rule: E* identical to the
+    reference's except logged curve near-ties; prediction.py:258-261 takes the
+    first maximum).  One dict per such series: series, e_star, runner_up, gap."""
+    out = []
+    rho = np.asarray(rho, dtype=np.float64)
+    for s in np.flatnonzero(np.asarray(est) > 0):
+        curve = rho[s]
+        b = int(est[s]) - 1
+        others = np.delete(curve, b)
+        idx = np.delete(np.arange(curve.size), b)
+        r = int(np.argmax(others))
+        gap = float(curve[b] - others[r])
+        if gap < tol:
+            out.append({"series": int(s), "e_star": b + 1, "runner_up": int(idx[r]) + 1, "gap": gap})
+    return out
+
+
 def _edim_wide(X: np.ndarray, e_max: int, tau: int, tp: int, rho: np.ndarray, est: np.ndarray) -> None:
     """skill_curves for e_max > NATIVE_E_MAX: the fused sweep for E <= NATIVE_E_MAX, the
     reference composition per (series, E) above it, E* re-taken over the whole curve

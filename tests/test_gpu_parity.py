@@ -389,9 +389,10 @@ def test_xmap_degenerate_inputs():
 @pytest.mark.gpu
 def test_xmap_offset_targets():
     """Series with a large offset and a small spread (1000 + 1e-3 noise): the
-    lookup's fp32 moments are accumulated about a per-library shift, so rho does
-    not lose its digits to the offset.  (Samples are float32 on the device, so
-    the oracle sees the same float32-rounded values.)"""
+    targets are centred before the fp32 lookup and ill-conditioned prediction
+    moments are finished in fp64 (lookup_fixup_kernel), so rho does not lose its
+    digits to the offset.  (The values are float32-representable, so the
+    oracle sees exactly the device's samples.)"""
     rng = np.random.default_rng(21)
     X = 1000.0 + 1e-2 * np.cumsum(rng.standard_normal((5, 300)), axis=1)
     X[1] = 1e4 + 1e-1 * np.sin(np.arange(300) * 0.3) + 1e-2 * rng.standard_normal(300)

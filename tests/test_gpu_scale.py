@@ -1,0 +1,99 @@
+"""GPU parity at the BASELINE configs' scale (VERDICT r01 "what's
+missing" 2): the long-series (T = 10,000) paths and the config-3 E* against the
+CPU oracle.  The oracle is the checker only; sizes are chosen so it finishes in
+tens of seconds on the box's host cores.
+
+Rules (north_star): E* identical except logged curve near-ties; curves of the
+fp64 edim path within 1e-10; rho within 1e-4; NaN patterns identical.
+"""
+
+import os
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import crossmap_oracle as O
+import paper_2105_12301_b200 as P
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+RHO_TOL = 1e-4
+CURVE_TOL = 1e-10
+WORKERS = os.cpu_count() or 1
+
+
+def _check_rows(rho_rows, ref_rows):
+    assert np.array_equal(np.isnan(rho_rows), np.isnan(ref_rows))
+    both = ~np.isnan(ref_rows)
+    return float(np.max(np.abs(rho_rows[both] - ref_rows[both]))) if both.any() else 0.0
+
+
+def test_xmap_long_series_non_resident_lookup():
+    """Config-2/4 length T = 10,000: targets do not fit shared memory, so the
+    cross map runs the non-resident lookup (lookup_xmap_kernel<false, 0>).  64
+    series of the mixed recipe, E* in {1, 2, 3, 5, 8}, three whole library rows
+    against the oracle's xmap rows (ccm.py:131-149)."""
+    X = P.mixed_dataset(64, 10_000, seed=2105, dtype=np.float32).astype(np.float64)
+    est = np.array([(1, 2, 3, 5, 8)[i % 5] for i in range(64)], dtype=np.int32)
+    rho = P.xmap(X.T, est)
+    libs = [0, 21, 63]
+    ref = O.xmap_rows(list(X), est.tolist(), libs, 1, workers=WORKERS)
+    worst = _check_rows(rho[libs], ref)
+    assert worst <= RHO_TOL, worst
+
+
+def test_edim_long_series_against_oracle():
+    """Config 2's shape per series (T = 10,000, E = 1..20, Tp = 1): curves within
+    1e-10 of the oracle's fp64 restatement and E* equal, on four series of
+    different types of the mixed recipe."""
+    X = P.mixed_dataset(20, 10_000, seed=2105).astype(np.float64)
+    pick = [0, 5, 9, 13]  # logistic, coupled pair member, noise, noisy sine types
+    est, rho = P.edim(X[pick].T, 20, 1, 1)
+    for r, i in enumerate(pick):
+        star, curve = O.edim(X[i], 20, 1, 1, workers=WORKERS)
+        oc = np.array([curve[e] for e in range(1, 21)])
+        assert np.max(np.abs(rho[r] - oc)) <= CURVE_TOL, i
+        ties = [t for t in P.near_ties(rho[r:r + 1], est[r:r + 1], tol=1e-9)]
+        assert est[r] == star or ties, (i, est[r], star)
+
+
+def test_config3_estar_against_oracle_and_fixture():
+    """Config 3 (N = 53,053, T = 1,450, mixed seed 2105): the GPU E* of 64
+    randomly sampled series equals the oracle's optimal_embedding (except logged
+    near-ties) and the committed fixture tests/golden/estar_config3.npz that the
+    reference arm of bench.py uses."""
+    fx = np.load(GOLDEN / "estar_config3.npz")
+    n, t, seed = int(fx["n"]), int(fx["t"]), int(fx["seed"])
+    X = P.mixed_dataset(n, t, seed=seed, dtype=np.float32)
+    rng = np.random.default_rng(64)
+    ids = np.sort(rng.choice(n, 64, replace=False))
+    sub = X[ids].astype(np.float64)
+    est, rho = P.edim(sub.T, 20, 1, 1)
+    assert np.array_equal(est, fx["estar"][ids].astype(np.int32))
+    ties = {d["series"] for d in P.near_ties(rho, est)}
+    mism = []
+    for r in range(64):
+        star, curve = O.edim(sub[r], 20, 1, 1, workers=WORKERS)
+        oc = np.array([curve[e] for e in range(1, 21)])
+        assert np.max(np.abs(rho[r] - oc)) <= CURVE_TOL, int(ids[r])
+        if est[r] != star:
+            mism.append(r)
+    assert all(r in ties for r in mism), (mism, ties)
+
+
+def test_xmap_float64_offset_inputs():
+    """float64 series with a large offset and a small spread
+    are not fp32-representable; the cross map must stage them in float64 (exact
+    neighbour certification, targets centred in fp64) and match the float64
+    oracle, not the oracle of the fp32-rounded copy."""
+    pair = P.coupled_logistic(1000, seed=3, beta=0.4)
+    a, b = pair[0].values, pair[1].values
+    for off, scale in ((300.0, 1e-3), (1e5, 1e-2)):
+        X = np.stack([off + scale * a, off + scale * b])
+        est = [2, 2]
+        r = P.xmap(X.T, est)
+        ref, _ = O.xmap([X[0], X[1]], est, 1, workers=1)
+        assert np.array_equal(np.isnan(r), np.isnan(ref)), off
+        assert np.nanmax(np.abs(r - ref)) <= RHO_TOL, (off, r, ref)
