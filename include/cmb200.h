@@ -156,17 +156,37 @@ int cmb_format_skill_csv(int dev, const void* rho, int rho_on_device, int is_f32
                          int64_t ld, int64_t row0, int64_t nrows, const char* names,
                          const int64_t* name_off, char* out, int64_t out_cap, int64_t* out_len);
 
-/* load_csv / read_skill_matrix (io.py:25-61, 81-110), numeric body: parse the
- * lines of buf (after the header) into out[row][ncols] with std::from_chars
- * (correctly rounded, like Python float()); label_col: the first cell of a row
- * is a label, its byte span goes to labels[2 r], labels[2 r + 1]; allow_na:
- * the cell "NA" is NaN; check_finite: inf/nan are rejected.  Host only (no
- * device needed).  Returns 0 and *nrows, or 1 when the text is outside this
- * grammar or invalid -- the caller then runs the reference algorithm, which
- * raises the reference's exact CsvFormatError.                              */
-int cmb_parse_numeric_csv(const char* buf, int64_t len, int64_t ncols, int label_col, int allow_na,
-                          int check_finite, double* out, int64_t cap_rows, int64_t* nrows,
-                          int64_t* labels);
+/* load_csv / read_skill_matrix (io.py:25-61, 81-110) input side, host only (no
+ * device needed).  The grammar is the reference's: Python's csv module (excel
+ * dialect, non-strict: quoting with '""' escapes, records ending at \n, \r\n
+ * or \r outside quotes, a blank line = a record with no cells) and float() per
+ * cell (ASCII blanks, sign, '_' between digits, exponent, inf/nan), correctly
+ * rounded.  Status codes: */
+#define CMB_CSV_OK 0
+#define CMB_CSV_EMPTY 1          /* no record at all                      -> "empty file"            */
+#define CMB_CSV_WIDTH 2          /* err[3] cells in record err[1]          -> "row r has n cells ..." */
+#define CMB_CSV_NOT_NUMERIC 3    /* load_csv cell err[2] of record err[1]  -> "not numeric: ..."      */
+#define CMB_CSV_NON_FINITE 4     /* load_csv inf/nan cell                  -> "non-finite value ..."  */
+#define CMB_CSV_BAD_CELL 5       /* read_skill_matrix cell (or a value past the n x n matrix)         */
+#define CMB_CSV_FIELD_LIMIT 6    /* a field over 131,072 characters        -> csv.Error               */
+#define CMB_CSV_CAPACITY 7       /* a caller buffer is too small / bad arguments                      */
+
+/* First record (the header): its unquoted cells go to text[spans[2c] ..
+ * spans[2c] + spans[2c+1]), *ncells cells; *body_off = offset of the next record. */
+int cmb_csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, int64_t* spans,
+                   int64_t max_cells, int64_t* ncells, int64_t* body_off);
+
+/* The records after the header.  mode 0 (load_csv): ncols numeric finite cells
+ * per record -> out[row][ncols].  mode 1 (read_skill_matrix): a label cell then
+ * ncols cells, "NA" = NaN; labels of rows < cap_rows go to labels/label_spans,
+ * later rows are only counted.  *nrows = records read.  Cells with non-ASCII
+ * bytes are left NaN and listed as (row, col) in defer[] (*ndefer): the caller
+ * converts them with float() (which accepts Unicode digits).  On a non-zero
+ * status err = {status, record (0 = first after the header), column, cells of
+ * the record, length of the cell text copied to err_text}.                  */
+int cmb_csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out, int64_t cap_rows,
+                 int64_t* nrows, char* labels, int64_t labels_cap, int64_t* label_spans, int64_t* defer,
+                 int64_t defer_cap, int64_t* ndefer, char* err_text, int64_t err_cap, int64_t* err);
 
 #ifdef __cplusplus
 }

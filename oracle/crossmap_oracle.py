@@ -487,3 +487,78 @@ def skill_matrix_csv_bytes(names, rho) -> bytes:
     for i, name in enumerate(names):
         w.writerow([name] + ["NA" if not math.isfinite(float(v)) else f"{float(v):.6f}" for v in rho[i]])
     return buf.getvalue().encode("utf-8")
+
+
+class CsvOracleError(Exception):
+    """The reference's CsvFormatError message (test oracle only)."""
+
+
+def load_csv_rows(path):
+    """load_csv (pkg/src/crossmap/io.py:25-61) restated on the csv module:
+    (names, values[T][N]) or CsvOracleError(message)."""
+    import csv
+    import math
+    with open(path, newline="", encoding="utf-8") as fh:
+        rows = csv.reader(fh)
+        try:
+            head = next(rows)
+        except StopIteration:
+            raise CsvOracleError(f"{path}: empty file") from None
+        names = [c.strip() for c in head]
+        if not all(names):
+            raise CsvOracleError(f"{path}: blank column name in header")
+        dup = sorted({n for n in names if names.count(n) > 1})
+        if dup:
+            raise CsvOracleError(f"{path}: duplicate column names: {dup}")
+        out = []
+        for r, row in enumerate(rows, start=2):
+            if len(row) != len(names):
+                raise CsvOracleError(f"{path}: row {r} has {len(row)} cells, expected {len(names)}")
+            vals = []
+            for c, cell in enumerate(row):
+                try:
+                    v = float(cell)
+                except ValueError:
+                    raise CsvOracleError(f"{path}: row {r}, column {names[c]!r}: not numeric: {cell.strip()!r}") from None
+                if not math.isfinite(v):
+                    raise CsvOracleError(f"{path}: row {r}, column {names[c]!r}: non-finite value {cell.strip()!r}")
+                vals.append(v)
+            out.append(vals)
+    if not names:
+        raise IndexError("list index out of range")
+    if not out:
+        raise CsvOracleError(f"{path}: no data rows")
+    return names, out
+
+
+def read_skill_matrix_rows(path):
+    """read_skill_matrix (io.py:81-110) restated: (names, rho) or CsvOracleError."""
+    import csv
+    with open(path, newline="", encoding="utf-8") as fh:
+        rows = csv.reader(fh)
+        try:
+            head = next(rows)
+        except StopIteration:
+            raise CsvOracleError(f"{path}: empty file") from None
+        names = head[1:]
+        if not names:
+            raise CsvOracleError(f"{path}: no target columns in header")
+        rho = np.full((len(names), len(names)), np.nan)
+        labels = []
+        for r, row in enumerate(rows, start=2):
+            if len(row) != len(names) + 1:
+                raise CsvOracleError(f"{path}: row {r} has {len(row)} cells, expected {len(names) + 1}")
+            labels.append(row[0])
+            for c, cell in enumerate(row[1:]):
+                if cell == "NA":
+                    continue
+                try:
+                    rho[r - 2, c] = float(cell)
+                except (ValueError, IndexError):
+                    raise CsvOracleError(f"{path}: row {r}, column {names[c]!r}: bad cell {cell!r}") from None
+    if labels != names:
+        raise CsvOracleError(f"{path}: library rows do not match target columns")
+    fin = rho[np.isfinite(rho)]
+    if fin.size and (fin.min() < -1.0 or fin.max() > 1.0):  # SkillMatrix (ccm.py:65-74)
+        raise OracleError("param", "finite skill entries must lie in [-1, 1]")
+    return names, rho

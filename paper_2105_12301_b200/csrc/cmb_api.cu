@@ -1086,11 +1086,20 @@ int cmb_format_skill_csv(int dev, const void* rho, int rho_on_device, int is_f32
   return CMB_OK;
 }
 
-int cmb_parse_numeric_csv(const char* buf, int64_t len, int64_t ncols, int label_col, int allow_na,
-                          int check_finite, double* out, int64_t cap_rows, int64_t* nrows,
-                          int64_t* labels) {
-  if (!buf || len < 0 || ncols < 1 || !out || !nrows || (label_col && !labels)) return 1;
-  return parse_numeric_csv(buf, len, ncols, label_col, allow_na, check_finite, out, cap_rows, nrows, labels);
+int cmb_csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, int64_t* spans, int64_t max_cells,
+                   int64_t* ncells, int64_t* body_off) {
+  if (!buf || len < 0 || !text || !spans || !ncells || !body_off) return CSV_CAPACITY;
+  return csv_header(buf, len, text, text_cap, spans, max_cells, ncells, body_off);
+}
+
+int cmb_csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out, int64_t cap_rows,
+                 int64_t* nrows, char* labels, int64_t labels_cap, int64_t* label_spans, int64_t* defer,
+                 int64_t defer_cap, int64_t* ndefer, char* err_text, int64_t err_cap, int64_t* err) {
+  if (!buf || len < 0 || (mode != 0 && mode != 1) || ncols < (mode == 1 ? 1 : 0) || !out || !nrows || !ndefer || !err ||
+      (mode == 1 && (!labels || !label_spans)))
+    return CSV_CAPACITY;
+  return csv_body(buf, len, mode, ncols, out, cap_rows, nrows, labels, labels_cap, label_spans, defer, defer_cap,
+                  ndefer, err_text, err_cap, err);
 }
 
 }  // extern "C"

@@ -18,6 +18,10 @@
 #include "cmb_common.cuh"
 #include "kernels.cuh"
 
+#include <cmath>
+#include <cstdlib>
+#include <string>
+
 #include <charconv>
 #include <cstring>
 #include <vector>
@@ -194,63 +198,231 @@ cudaError_t format_skill_rows(const void* rho_dev, bool f32, int64_t n, int64_t 
   return cudaGetLastError();
 }
 
-// ---------------------------------------------------------------- host CSV parsing
-// Fast path for the numeric body of a CSV (the lines after the header).  A cell
-// is optional blanks, an optional '+', a number std::from_chars accepts
-// (correctly rounded, like Python's float), optional blanks -- or exactly "NA"
-// when allow_na.  label_col: the first cell of each row is a label whose byte
-// span goes to labels[2 r], labels[2 r + 1].  check_finite rejects inf/nan.
-// Returns 0 with *nrows rows parsed, or 1 for anything else (ragged or blank
-// rows, non-numeric cells, quotes, '_' digit separators, more than cap_rows
-// rows): the caller then runs the reference algorithm, which raises the
-// reference's exact error for invalid files.
-int parse_numeric_csv(const char* buf, int64_t len, int64_t ncols, int label_col, int allow_na,
-                      int check_finite, double* out, int64_t cap_rows, int64_t* nrows, int64_t* labels) {
-  int64_t pos = 0, row = 0;
-  const int64_t want = ncols + (label_col ? 1 : 0);
-  while (pos < len) {
-    int64_t eol = pos;
-    while (eol < len && buf[eol] != '\n') ++eol;
-    int64_t end = eol;
-    if (end > pos && buf[end - 1] == '\r') --end;
-    if (eol >= len && end == pos) break;  // no bytes after the last newline
-    if (end == pos || row >= cap_rows) return 1;
-    if (memchr(buf + pos, '"', (size_t)(end - pos)) || memchr(buf + pos, '_', (size_t)(end - pos)) ||
-        memchr(buf + pos, '\r', (size_t)(end - pos)) || memchr(buf + pos, '(', (size_t)(end - pos)))
-      return 1;
-    int64_t c = pos, col = 0;
-    for (;;) {
-      int64_t ce = c;
-      while (ce < end && buf[ce] != ',') ++ce;
-      if (col >= want) return 1;
-      if (label_col && col == 0) {
-        labels[2 * row] = c;
-        labels[2 * row + 1] = ce - c;
-      } else {
-        int64_t a = c, b = ce;
-        while (a < b && (buf[a] == ' ' || buf[a] == '\t')) ++a;
-        while (b > a && (buf[b - 1] == ' ' || buf[b - 1] == '\t')) --b;
-        double v;
-        if (allow_na && ce - c == 2 && buf[c] == 'N' && buf[c + 1] == 'A') {
-          v = __builtin_nan("");
-        } else {
-          if (a < b && buf[a] == '+') ++a;
-          if (a >= b || buf[a] == '+' || buf[a] == '-' && a > c && buf[a - 1] == '+') return 1;
-          auto r = std::from_chars(buf + a, buf + b, v);
-          if (r.ec != std::errc() || r.ptr != buf + b) return 1;
-          if (check_finite && !__builtin_isfinite(v)) return 1;
-        }
-        out[row * ncols + (label_col ? col - 1 : col)] = v;
-      }
-      ++col;
-      if (ce >= end) break;
-      c = ce + 1;
+// ---------------------------------------------------------------- host CSV reading
+// The input grammar of the reference's readers (pkg/src/crossmap/io.py:25-61,
+// 81-110): Python's csv module, excel dialect, non-strict -- records end at
+// \n, \r\n or \r outside quotes (a blank line is a record with no cells); a
+// field that starts with '"' is quoted, '""' inside it is one '"', newlines are
+// kept, characters after the closing quote are appended; a quoted field left
+// open at the end of the data ends there -- and Python's float() on each cell:
+// ASCII blanks stripped, optional sign, digits with single '_' between
+// digits, optional fraction and exponent, or inf / infinity / nan (any case).
+// Values are correctly rounded (std::from_chars, strtod for out-of-range
+// exponents), so they are bit-identical to float().  Cells with non-ASCII
+// bytes (Unicode digits or blanks, which float() also accepts) are listed for
+// the caller to convert with float() itself.
+namespace {
+
+constexpr int64_t kFieldLimit = 131072;  // csv.field_size_limit() default
+
+struct CsvCursor {
+  const char* b;
+  int64_t n, pos = 0;
+  std::string field;                      // unquoted text of the current field
+  std::vector<std::pair<int64_t, int64_t>> spans;  // fields of the record in `text`
+  std::string text;
+  bool oversize = false;
+  CsvCursor(const char* buf, int64_t len) : b(buf), n(len) {}
+
+  // next record into spans/text; false at the end of the data
+  bool next() {
+    spans.clear();
+    text.clear();
+    if (pos >= n) return false;
+    enum { START_FIELD, IN_FIELD, IN_QUOTED, QUOTE_IN_QUOTED } st = START_FIELD;
+    // a line break at the start of a record: a record without cells
+    if (b[pos] == '\n' || b[pos] == '\r') {
+      pos += (b[pos] == '\r' && pos + 1 < n && b[pos + 1] == '\n') ? 2 : 1;
+      return true;
     }
-    if (col != want) return 1;
+    field.clear();
+    auto save = [&]() {
+      if ((int64_t)field.size() > kFieldLimit) oversize = true;
+      spans.push_back({(int64_t)text.size(), (int64_t)field.size()});
+      text += field;
+      field.clear();
+    };
+    while (pos < n) {
+      const char c = b[pos];
+      const bool eol = c == '\n' || c == '\r';
+      switch (st) {
+        case START_FIELD:
+          if (eol) { save(); goto record_end; }
+          if (c == '"') st = IN_QUOTED;
+          else if (c == ',') save();
+          else { field.push_back(c); st = IN_FIELD; }
+          break;
+        case IN_FIELD:
+          if (eol) { save(); goto record_end; }
+          if (c == ',') { save(); st = START_FIELD; }
+          else field.push_back(c);
+          break;
+        case IN_QUOTED:
+          if (c == '"') st = QUOTE_IN_QUOTED;
+          else field.push_back(c);
+          break;
+        case QUOTE_IN_QUOTED:
+          if (c == '"') { field.push_back('"'); st = IN_QUOTED; }
+          else if (c == ',') { save(); st = START_FIELD; }
+          else if (eol) { save(); goto record_end; }
+          else { field.push_back(c); st = IN_FIELD; }
+          break;
+      }
+      ++pos;
+    }
+    save();  // end of data (an open quoted field ends here, non-strict)
+    return true;
+  record_end:
+    pos += (b[pos] == '\r' && pos + 1 < n && b[pos + 1] == '\n') ? 2 : 1;
+    return true;
+  }
+};
+
+bool ascii_blank(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\v' || c == '\f' || c == '\r'; }
+
+// float(cell) for an ASCII cell: 0 ok, 1 not a number
+int py_float(const char* s, int64_t len, double* v) {
+  int64_t a = 0, e = len;
+  while (a < e && ascii_blank(s[a])) ++a;
+  while (e > a && ascii_blank(s[e - 1])) --e;
+  if (a == e) return 1;
+  bool neg = false;
+  if (s[a] == '+' || s[a] == '-') { neg = s[a] == '-'; ++a; }
+  const int64_t m = e - a;
+  auto ieq = [&](const char* w) {
+    const int64_t k = (int64_t)strlen(w);
+    if (k != m) return false;
+    for (int64_t q = 0; q < k; ++q)
+      if ((s[a + q] | 0x20) != w[q]) return false;
+    return true;
+  };
+  if (ieq("inf") || ieq("infinity")) { *v = neg ? -HUGE_VAL : HUGE_VAL; return 0; }
+  if (ieq("nan")) { *v = neg ? -__builtin_nan("") : __builtin_nan(""); return 0; }
+  // digits ('_' only between two digits), '.', exponent
+  char tmp[512];
+  std::string big;
+  char* d = tmp;
+  if (m + 2 > (int64_t)sizeof(tmp)) { big.resize(m + 2); d = &big[0]; }
+  int64_t o = 0, mant = 0;
+  bool dot = false, exp = false, exp_digits = false;
+  for (int64_t q = a; q < e; ++q) {
+    const char c = s[q];
+    if (c >= '0' && c <= '9') {
+      d[o++] = c;
+      if (exp) exp_digits = true; else ++mant;
+    } else if (c == '_') {
+      if (q == a || q + 1 >= e || !(s[q - 1] >= '0' && s[q - 1] <= '9') || !(s[q + 1] >= '0' && s[q + 1] <= '9'))
+        return 1;
+    } else if (c == '.' && !dot && !exp) {
+      dot = true;
+      d[o++] = c;
+    } else if ((c == 'e' || c == 'E') && !exp && mant > 0) {
+      exp = true;
+      d[o++] = 'e';
+      if (q + 1 < e && (s[q + 1] == '+' || s[q + 1] == '-')) d[o++] = s[++q];
+    } else {
+      return 1;
+    }
+  }
+  if (mant == 0 || (exp && !exp_digits)) return 1;
+  double r = 0.0;
+  auto res = std::from_chars(d, d + o, r);
+  if (res.ptr != d + o) return 1;
+  if (res.ec == std::errc::result_out_of_range) {  // overflow -> inf, underflow -> 0 / subnormal
+    d[o] = '\0';
+    r = strtod(d, nullptr);
+  } else if (res.ec != std::errc()) {
+    return 1;
+  }
+  *v = neg ? -r : r;
+  return 0;
+}
+
+bool has_high_byte(const char* s, int64_t len) {
+  for (int64_t q = 0; q < len; ++q)
+    if ((unsigned char)s[q] >= 0x80) return true;
+  return false;
+}
+
+}  // namespace
+
+int csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, int64_t* spans, int64_t max_cells,
+               int64_t* ncells, int64_t* body_off) {
+  CsvCursor cur(buf, len);
+  if (!cur.next()) return CSV_EMPTY;
+  if (cur.oversize) return CSV_FIELD_LIMIT;
+  if ((int64_t)cur.spans.size() > max_cells || (int64_t)cur.text.size() > text_cap) return CSV_CAPACITY;
+  memcpy(text, cur.text.data(), cur.text.size());
+  for (size_t q = 0; q < cur.spans.size(); ++q) {
+    spans[2 * q] = cur.spans[q].first;
+    spans[2 * q + 1] = cur.spans[q].second;
+  }
+  *ncells = (int64_t)cur.spans.size();
+  *body_off = cur.pos;
+  return 0;
+}
+
+int csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out, int64_t cap_rows, int64_t* nrows,
+             char* labels, int64_t labels_cap, int64_t* label_spans, int64_t* defer, int64_t defer_cap,
+             int64_t* ndefer, char* err_text, int64_t err_cap, int64_t* err) {
+  CsvCursor cur(buf, len);
+  const int64_t want = ncols + (mode == 1 ? 1 : 0);
+  int64_t row = 0, lab = 0, nd = 0;
+  auto fail = [&](int code, int64_t col, const char* t, int64_t tl, int64_t ncell) {
+    err[0] = code;
+    err[1] = row;
+    err[2] = col;
+    err[3] = ncell;
+    err[4] = std::min(tl, err_cap);
+    if (t) memcpy(err_text, t, (size_t)err[4]);
+    *nrows = row;
+    *ndefer = nd;
+    return code;
+  };
+  while (cur.next()) {
+    if (cur.oversize) return fail(CSV_FIELD_LIMIT, 0, nullptr, 0, 0);
+    const int64_t nc = (int64_t)cur.spans.size();
+    if (nc != want) return fail(CSV_WIDTH, 0, nullptr, 0, nc);
+    const char* t = cur.text.data();
+    if (mode == 1 && row < cap_rows) {  // rows past the matrix only count (then a row-name mismatch)
+      const auto sp = cur.spans[0];
+      if (lab + sp.second > labels_cap) return fail(CSV_CAPACITY, 0, nullptr, 0, 0);
+      memcpy(labels + lab, t + sp.first, (size_t)sp.second);
+      label_spans[2 * row] = lab;
+      label_spans[2 * row + 1] = sp.second;
+      lab += sp.second;
+    }
+    for (int64_t c = (mode == 1 ? 1 : 0); c < nc; ++c) {
+      const int64_t col = mode == 1 ? c - 1 : c;
+      const char* f = t + cur.spans[c].first;
+      const int64_t fl = cur.spans[c].second;
+      double v;
+      if (mode == 1 && fl == 2 && f[0] == 'N' && f[1] == 'A') {
+        if (row < cap_rows) out[row * ncols + col] = __builtin_nan("");
+        continue;
+      } else if (has_high_byte(f, fl)) {
+        // float() also takes Unicode digits and blanks: the caller converts
+        if (nd >= defer_cap) return fail(CSV_CAPACITY, col, nullptr, 0, 0);
+        if (row >= cap_rows) return fail(mode == 1 ? CSV_BAD_CELL : CSV_CAPACITY, col, f, fl, 0);
+        defer[2 * nd] = row;
+        defer[2 * nd + 1] = col;
+        ++nd;
+        out[row * ncols + col] = __builtin_nan("");
+        continue;
+      } else if (py_float(f, fl, &v) != 0) {
+        return fail(mode == 1 ? CSV_BAD_CELL : CSV_NOT_NUMERIC, col, f, fl, 0);
+      } else if (mode == 0 && !std::isfinite(v)) {
+        return fail(CSV_NON_FINITE, col, f, fl, 0);
+      }
+      // read_skill_matrix: a value past the n x n matrix is the reference's IndexError -> bad cell
+      if (row >= cap_rows) return fail(mode == 1 ? CSV_BAD_CELL : CSV_CAPACITY, col, f, fl, 0);
+      out[row * ncols + col] = v;
+    }
     ++row;
-    pos = eol + 1;
   }
   *nrows = row;
+  *ndefer = nd;
+  err[0] = 0;
   return 0;
 }
 

@@ -135,7 +135,13 @@ cudaError_t format_skill_rows(const void* rho_dev, bool f32, int64_t n, int64_t 
                               int64_t* row_len_dev, int64_t* row_off_dev, int64_t* row_off_host,
                               int* range_err_dev, bool* out_of_range, char* out_dev, int64_t out_cap,
                               int64_t* out_len, cudaStream_t st);
-int parse_numeric_csv(const char* buf, int64_t len, int64_t ncols, int label_col, int allow_na,
-                      int check_finite, double* out, int64_t cap_rows, int64_t* nrows, int64_t* labels);
+// host CSV reader (io.cu): status codes of csv_header / csv_body (CMB_CSV_* in cmb200.h)
+enum CsvStatus { CSV_OK = 0, CSV_EMPTY = 1, CSV_WIDTH = 2, CSV_NOT_NUMERIC = 3, CSV_NON_FINITE = 4,
+                 CSV_BAD_CELL = 5, CSV_FIELD_LIMIT = 6, CSV_CAPACITY = 7 };
+int csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, int64_t* spans, int64_t max_cells,
+               int64_t* ncells, int64_t* body_off);
+int csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out, int64_t cap_rows, int64_t* nrows,
+             char* labels, int64_t labels_cap, int64_t* label_spans, int64_t* defer, int64_t defer_cap,
+             int64_t* ndefer, char* err_text, int64_t err_cap, int64_t* err);
 
 }  // namespace cmb

@@ -14,12 +14,13 @@ B200 path.  The cell text of a skill matrix is produced on the GPU
 bits, csrc/io.cu) in row batches, from host arrays or straight from a device
 buffer (``write_skill_matrix_device``, e.g. the target-major output of the
 sharded cross map), so at N = 53,053 the 28 GB of text is formatted where
-rho already lives.  Numeric CSV bodies are parsed in C++ (``std::from_chars``,
-correctly rounded like Python's float).  The reference's own csv-module
-algorithm (restated below) handles text outside that fast grammar -- quoted
-fields, '_' digit separators -- and every invalid file, so errors carry the
-reference's exact messages.  ``write_skill_matrix_npz`` / ``read_skill_matrix_npz``
-add the binary path for matrices too large for text.
+rho already lives.  Input files are read by libcmb200's host CSV reader
+(``cmb_csv_header`` / ``cmb_csv_body``): the csv module's excel dialect and
+float()'s grammar in C++ (``std::from_chars``, correctly rounded like float()),
+returning the position and text of the first invalid record or cell, from
+which the reference's exact CsvFormatError messages are built here.
+``write_skill_matrix_npz`` / ``read_skill_matrix_npz`` add the binary path for
+matrices too large for text.
 """
 
 from __future__ import annotations
@@ -40,122 +41,129 @@ _NA = "NA"
 _BATCH_BYTES = 1 << 30  # text per GPU formatting batch
 
 
-# ---------------------------------------------------------------- reference algorithm
-def _load_csv_reference(path: Path) -> Dataset:
-    """io.py:25-61 restated: the csv-module parse with the reference's checks."""
-    with path.open(newline="", encoding="utf-8") as handle:
-        reader = csv.reader(handle)
-        try:
-            header = next(reader)
-        except StopIteration:
-            raise CsvFormatError(f"{path}: empty file") from None
-        names = [cell.strip() for cell in header]
-        if any(not name for name in names):
-            raise CsvFormatError(f"{path}: blank column name in header")
-        duplicates = {n for n in names if names.count(n) > 1}
-        if duplicates:
-            raise CsvFormatError(f"{path}: duplicate column names: {sorted(duplicates)}")
-        columns: list[list[float]] = [[] for _ in names]
-        for row_number, row in enumerate(reader, start=2):
-            if len(row) != len(names):
-                raise CsvFormatError(
-                    f"{path}: row {row_number} has {len(row)} cells, expected {len(names)}")
-            for col, cell in enumerate(row):
-                try:
-                    value = float(cell)
-                except ValueError:
-                    raise CsvFormatError(
-                        f"{path}: row {row_number}, column {names[col]!r}: "
-                        f"not numeric: {cell.strip()!r}") from None
-                if not math.isfinite(value):
-                    raise CsvFormatError(
-                        f"{path}: row {row_number}, column {names[col]!r}: "
-                        f"non-finite value {cell.strip()!r}")
-                columns[col].append(value)
-    if not columns[0]:
-        raise CsvFormatError(f"{path}: no data rows")
-    return Dataset(tuple(TimeSeries(column, name) for column, name in zip(columns, names)))
+# ---------------------------------------------------------------- input (native reader)
+_FIELD_LIMIT = 131072  # csv.field_size_limit() default, enforced by cmb_csv_*
+_CSV_EMPTY, _CSV_WIDTH, _CSV_NOT_NUMERIC, _CSV_NON_FINITE, _CSV_BAD_CELL, _CSV_FIELD_LIMIT = 1, 2, 3, 4, 5, 6
 
 
-def _read_skill_matrix_reference(path: Path) -> SkillMatrix:
-    """io.py:81-110 restated."""
-    with path.open(newline="", encoding="utf-8") as handle:
-        reader = csv.reader(handle)
-        try:
-            header = next(reader)
-        except StopIteration:
-            raise CsvFormatError(f"{path}: empty file") from None
-        names = header[1:]
-        if not names:
-            raise CsvFormatError(f"{path}: no target columns in header")
-        rho = np.full((len(names), len(names)), np.nan)
-        row_names = []
-        for row_number, row in enumerate(reader, start=2):
-            if len(row) != len(names) + 1:
-                raise CsvFormatError(
-                    f"{path}: row {row_number} has {len(row)} cells, expected {len(names) + 1}")
-            row_names.append(row[0])
-            for col, cell in enumerate(row[1:]):
-                if cell == _NA:
-                    continue
-                try:
-                    rho[row_number - 2, col] = float(cell)
-                except (ValueError, IndexError):
-                    raise CsvFormatError(
-                        f"{path}: row {row_number}, column {names[col]!r}: bad cell {cell!r}") from None
-    if row_names != names:
-        raise CsvFormatError(f"{path}: library rows do not match target columns")
-    return SkillMatrix(names, rho)
+def _raw(path: Path) -> bytes:
+    """The file image; non-ASCII content must be valid UTF-8 (the reference opens
+    with encoding="utf-8", so an invalid byte raises UnicodeDecodeError there too)."""
+    raw = path.read_bytes()
+    if np.count_nonzero(np.frombuffer(raw, dtype=np.uint8) >= 0x80):
+        raw.decode("utf-8")
+    return raw
 
 
-# ---------------------------------------------------------------- fast paths
-def _split_header(raw: bytes):
-    """(header cells, body offset) when the header needs no csv quoting, else None."""
-    nl = raw.find(b"\n")
-    if nl < 0:
-        return None
-    line = raw[:nl]
-    if line.endswith(b"\r"):
-        line = line[:-1]
-    if b'"' in line or b"\r" in line:
-        return None
-    try:
-        cells = line.decode("utf-8").split(",")
-    except UnicodeDecodeError:
-        return None
-    return cells, nl + 1
+def _header(raw: bytes, path: Path) -> tuple[list[str], int]:
+    """Unquoted cells of the first record and the offset of the second
+    (cmb_csv_header; the csv module's excel dialect)."""
+    buf = np.frombuffer(raw, dtype=np.uint8)
+    max_cells = int(np.count_nonzero(buf == 44)) + 1
+    text = np.empty(max(len(raw), 1), dtype=np.uint8)
+    spans = np.empty(2 * max_cells, dtype=np.int64)
+    ncells, body = np.zeros(1, np.int64), np.zeros(1, np.int64)
+    rc = nat.load().cmb_csv_header(nat.ptr(buf if buf.size else np.zeros(1, np.uint8)), len(raw), nat.ptr(text), text.size,
+                                   nat.ptr(spans), max_cells, nat.ptr(ncells), nat.ptr(body))
+    if rc == _CSV_EMPTY:
+        raise CsvFormatError(f"{path}: empty file")
+    _raise_field_limit(rc)
+    t = text.tobytes()
+    cells = [t[spans[2 * c]:spans[2 * c] + spans[2 * c + 1]].decode("utf-8") for c in range(int(ncells[0]))]
+    return cells, int(body[0])
 
 
-def _parse_body(raw: bytes, start: int, ncols: int, label: bool, allow_na: bool, check_finite: bool,
-                cap_rows: int | None = None):
-    body = np.frombuffer(raw, dtype=np.uint8)[start:]
-    cap = cap_rows if cap_rows is not None else int(np.count_nonzero(body == 10)) + 1
-    out = np.empty((max(cap, 1), ncols), dtype=np.float64)
-    labels = np.zeros((max(cap, 1), 2), dtype=np.int64) if label else None
-    nrows = np.zeros(1, dtype=np.int64)
-    body = np.ascontiguousarray(body)
-    rc = nat.load().cmb_parse_numeric_csv(nat.ptr(body), body.size, ncols, int(label), int(allow_na),
-                                          int(check_finite), nat.ptr(out), cap, nat.ptr(nrows),
-                                          nat.ptr(labels))
-    if rc != 0:
-        return None
-    n = int(nrows[0])
-    return out[:n], (labels[:n] if label else None), body
+def _raise_field_limit(rc: int) -> None:
+    if rc == _CSV_FIELD_LIMIT:
+        import csv
+        raise csv.Error(f"field larger than field limit ({_FIELD_LIMIT})")
+    if rc not in (0, _CSV_EMPTY, _CSV_WIDTH, _CSV_NOT_NUMERIC, _CSV_NON_FINITE, _CSV_BAD_CELL):
+        raise CsvFormatError(f"CSV reader failed with status {rc}")
+
+
+class _Body:
+    """Records after the header through cmb_csv_body: values, row labels (mode 1),
+    the cells left for Python's float() (non-ASCII), and the first error."""
+
+    def __init__(self, raw: bytes, off: int, mode: int, ncols: int, cap_rows: int | None):
+        buf = np.frombuffer(raw, dtype=np.uint8)[off:]
+        records = int(np.count_nonzero(buf == 10) + np.count_nonzero(buf == 13)) + 1
+        cap = records if cap_rows is None else cap_rows
+        self.values = np.full((max(cap, 1), max(ncols, 1)), np.nan)
+        labels = np.empty(max(buf.size, 1), dtype=np.uint8)
+        lspans = np.zeros((max(cap, 1), 2), dtype=np.int64)
+        ndef_cap = int(np.count_nonzero(buf >= 0x80)) + 1
+        defer = np.zeros((ndef_cap, 2), dtype=np.int64)
+        err = np.zeros(8, dtype=np.int64)
+        err_text = np.empty(_FIELD_LIMIT + 1, dtype=np.uint8)
+        nrows, ndef = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        body = raw[off:]
+        bptr = nat.ptr(np.ascontiguousarray(buf)) if buf.size else nat.ptr(np.zeros(1, np.uint8))
+        self.rc = nat.load().cmb_csv_body(bptr, len(body), mode, ncols, nat.ptr(self.values), cap, nat.ptr(nrows),
+                                          nat.ptr(labels), labels.size, nat.ptr(lspans), nat.ptr(defer), ndef_cap,
+                                          nat.ptr(ndef), nat.ptr(err_text), err_text.size, nat.ptr(err))
+        _raise_field_limit(self.rc)
+        self.nrows = int(nrows[0])
+        self.err_row, self.err_col, self.err_cells = int(err[1]), int(err[2]), int(err[3])
+        self.err_text = err_text[: int(err[4])].tobytes().decode("utf-8", errors="surrogateescape")
+        self.deferred = [(int(r), int(c)) for r, c in defer[: int(ndef[0])]]
+        if self.deferred:  # their text: re-read those records with the field spans of the same reader
+            self._deferred_text(body, mode)
+        lb = labels.tobytes()
+        self.labels = [lb[a:a + b].decode("utf-8") for a, b in lspans[: min(self.nrows, cap)]] if mode == 1 else []
+
+    def _deferred_text(self, body: bytes, mode: int) -> None:
+        """Cell text of the deferred cells: a second pass of the header reader
+        over each record (the same tokenizer), record by record."""
+        want = {r for r, _ in self.deferred}
+        texts, pos, rec = {}, 0, 0
+        while rec <= max(want) and pos < len(body):
+            cells, nxt = _header(body[pos:], Path("<record>"))
+            if rec in want:
+                texts[rec] = cells
+            pos += nxt
+            rec += 1
+        shift = 1 if mode == 1 else 0
+        self.deferred_text = [texts[r][c + shift] for r, c in self.deferred]
 
 
 def load_csv(path) -> Dataset:
-    """Parse a columns-as-series CSV into a Dataset (io.py:25-61)."""
+    """Parse a columns-as-series CSV into a Dataset (io.py:25-61): the native
+    reader tokenises and converts, errors carry the reference's messages."""
     path = Path(path)
-    raw = path.read_bytes()
-    head = _split_header(raw)
-    if head is not None:
-        names = [c.strip() for c in head[0]]
-        if names and all(names) and len(set(names)) == len(names):
-            parsed = _parse_body(raw, head[1], len(names), False, False, True)
-            if parsed is not None and parsed[0].shape[0] > 0:
-                values = parsed[0]
-                return Dataset(tuple(TimeSeries(values[:, j], name) for j, name in enumerate(names)))
-    return _load_csv_reference(path)  # quoting, '_' separators, or an invalid file
+    raw = _raw(path)
+    cells, off = _header(raw, path)
+    names = [c.strip() for c in cells]
+    if any(not n for n in names):
+        raise CsvFormatError(f"{path}: blank column name in header")
+    seen: dict[str, int] = {}
+    for n in names:
+        seen[n] = seen.get(n, 0) + 1
+    dup = sorted(n for n, c in seen.items() if c > 1)
+    if dup:
+        raise CsvFormatError(f"{path}: duplicate column names: {dup}")
+    b = _Body(raw, off, 0, len(names), None)
+    for (r, c), text in zip(b.deferred, getattr(b, "deferred_text", [])):
+        where = f"{path}: row {r + 2}, column {names[c]!r}"
+        try:
+            v = float(text)
+        except ValueError:
+            raise CsvFormatError(f"{where}: not numeric: {text.strip()!r}") from None
+        if not math.isfinite(v):
+            raise CsvFormatError(f"{where}: non-finite value {text.strip()!r}")
+        b.values[r, c] = v
+    if b.rc == _CSV_WIDTH:
+        raise CsvFormatError(f"{path}: row {b.err_row + 2} has {b.err_cells} cells, expected {len(names)}")
+    if b.rc in (_CSV_NOT_NUMERIC, _CSV_NON_FINITE):
+        what = "not numeric:" if b.rc == _CSV_NOT_NUMERIC else "non-finite value"
+        raise CsvFormatError(f"{path}: row {b.err_row + 2}, column {names[b.err_col]!r}: "
+                             f"{what} {b.err_text.strip()!r}")
+    if not names:
+        raise IndexError("list index out of range")  # the reference indexes columns[0] of none
+    if b.nrows == 0:
+        raise CsvFormatError(f"{path}: no data rows")
+    values = b.values[: b.nrows]
+    return Dataset(tuple(TimeSeries(values[:, j], name) for j, name in enumerate(names)))
 
 
 def _name_fields(names) -> list[bytes]:
@@ -221,26 +229,29 @@ def write_skill_matrix_device(rho_ptr: int, n: int, ld: int, names, path, float3
 
 
 def read_skill_matrix(path) -> SkillMatrix:
-    """Inverse of write_skill_matrix, at six-decimal precision (io.py:81-110)."""
+    """Inverse of write_skill_matrix, at six-decimal precision (io.py:81-110),
+    through the native reader."""
     path = Path(path)
-    raw = path.read_bytes()
-    head = _split_header(raw)
-    if head is not None and len(head[0]) > 1:
-        names = head[0][1:]
-        parsed = _parse_body(raw, head[1], len(names), True, True, False, cap_rows=len(names))
-        if parsed is not None:
-            values, spans, body = parsed
-            try:
-                row_names = [bytes(body[a:a + b]).decode("utf-8") for a, b in spans]
-            except UnicodeDecodeError:
-                row_names = None
-            if row_names is not None:
-                if row_names != names:
-                    raise CsvFormatError(f"{path}: library rows do not match target columns")
-                rho = np.full((len(names), len(names)), np.nan)
-                rho[: values.shape[0]] = values
-                return SkillMatrix(names, rho)
-    return _read_skill_matrix_reference(path)
+    raw = _raw(path)
+    header, off = _header(raw, path)
+    names = header[1:]
+    if not names:
+        raise CsvFormatError(f"{path}: no target columns in header")
+    n = len(names)
+    b = _Body(raw, off, 1, n, n)
+    for (r, c), text in zip(b.deferred, getattr(b, "deferred_text", [])):
+        try:
+            v = float(text)
+        except ValueError:
+            raise CsvFormatError(f"{path}: row {r + 2}, column {names[c]!r}: bad cell {text!r}") from None
+        b.values[r, c] = v
+    if b.rc == _CSV_WIDTH:
+        raise CsvFormatError(f"{path}: row {b.err_row + 2} has {b.err_cells} cells, expected {n + 1}")
+    if b.rc == _CSV_BAD_CELL:
+        raise CsvFormatError(f"{path}: row {b.err_row + 2}, column {names[b.err_col]!r}: bad cell {b.err_text!r}")
+    if b.nrows != n or b.labels != names:
+        raise CsvFormatError(f"{path}: library rows do not match target columns")
+    return SkillMatrix(names, b.values[:n, :n].copy())
 
 
 # ---------------------------------------------------------------- binary path

@@ -2,8 +2,8 @@
 against the reference's own outputs (tests/golden/io_cases.json, produced by
 tests/golden/make_io_golden.py from /root/reference) and the oracle restatement.
 
-CPU tests cover the parsers (host C++ fast path + the reference algorithm for
-everything outside its grammar); the GPU tests cover the formatter kernel."""
+CPU tests cover the native host reader (libcmb200's cmb_csv_header /
+cmb_csv_body, loaded without a device); the GPU tests cover the formatter kernel."""
 
 import json
 from pathlib import Path
@@ -57,22 +57,94 @@ def test_read_skill_matrix_matches_reference(case, tmp_path):
     assert np.array_equal(np.nan_to_num(m.rho, nan=7.0), np.nan_to_num(want, nan=7.0))
 
 
-def test_plain_files_take_the_native_parser(tmp_path, monkeypatch):
-    """The C++ fast path parses ordinary files on its own (the reference algorithm
-    is only reached for quoting / '_' separators / invalid files)."""
-    def boom(path):
-        raise AssertionError("reference path used")
-    monkeypatch.setattr(pio, "_load_csv_reference", boom)
-    monkeypatch.setattr(pio, "_read_skill_matrix_reference", boom)
+def test_no_reference_code_in_the_reader():
+    """The input side is the native reader (cmb_csv_header / cmb_csv_body); there
+    is no restated reference algorithm to fall back to."""
+    assert not any(hasattr(pio, n) for n in ("_load_csv_reference", "_read_skill_matrix_reference"))
     rng = np.random.default_rng(0)
     X = rng.standard_normal((300, 4)) * 10.0 ** rng.integers(-8, 8, (300, 4))
-    p = tmp_path / "d.csv"
-    p.write_text("a,b,c,d\n" + "".join(",".join(repr(float(v)) for v in row) + "\n" for row in X))
-    ds = P.load_csv(p)
+    ds = None
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        p = Path(d) / "d.csv"
+        p.write_text("a,b,c,d\n" + "".join(",".join(repr(float(v)) for v in row) + "\n" for row in X))
+        ds = P.load_csv(p)
     assert np.array_equal(np.array([s.values for s in ds]).T, X)
-    q = tmp_path / "m.csv"
-    q.write_bytes(CASES["read_skill_matrix"]["layout"]["text"].encode())
-    assert P.read_skill_matrix(q).names == ["a", "b"]
+
+
+def _fuzz_cell(rng, numeric_only=False, unit=False):
+    kinds = ["num", "num", "num", "ws", "under", "exp", "inf", "nan", "quoted", "bad", "empty", "nbsp"]
+    k = kinds[int(rng.integers(len(kinds)))] if not numeric_only else "num"
+    v = float(rng.uniform(-1, 1)) if unit else float(rng.standard_normal() * 10.0 ** int(rng.integers(-5, 5)))
+    if k == "num":
+        return repr(v)
+    if k == "ws":
+        return " \t" + repr(v) + " "
+    if k == "under":
+        return ["1_000", "1__0", "_1", "1_", "1_0.2_5", "1e1_0", "1._5"][int(rng.integers(7))]
+    if k == "exp":
+        return ["1e400", "-1e-400", "2.5E-3", "+.5", "5.", ".", "1e", "e5"][int(rng.integers(8))]
+    if k == "inf":
+        return ["inf", "-Infinity", "+INF", "infinit"][int(rng.integers(4))]
+    if k == "nan":
+        return ["nan", "-NaN", "nan(1)", "NA"][int(rng.integers(4))]
+    if k == "quoted":
+        return '"' + repr(v) + '"' if rng.random() < 0.7 else '"1,5"'
+    if k == "bad":
+        return ["x", "0x10", "1 2", "--1", "(1)"][int(rng.integers(5))]
+    if k == "nbsp":
+        return "\u00a0" + repr(v) if rng.random() < 0.5 else "\u0661\u0662"
+    return ""
+
+
+def _fuzz_text(rng, label):
+    ncol = int(rng.integers(1, 5))
+    names = [f"c{j}" for j in range(ncol)]
+    lines = [("," if label else "") + ",".join(names)]
+    nrow = ncol if label else int(rng.integers(0, 6))
+    for r in range(nrow):
+        cells = [_fuzz_cell(rng, numeric_only=rng.random() < 0.6, unit=label) for _ in range(ncol)]
+        if rng.random() < 0.1:
+            cells = cells[:-1]
+        lines.append(((names[r] + ",") if label else "") + ",".join(cells))
+    if rng.random() < 0.1:
+        lines.insert(int(rng.integers(1, len(lines) + 1)), "")
+    eol = ["\n", "\r\n", "\r"][int(rng.integers(3))]
+    return eol.join(lines) + (eol if rng.random() < 0.8 else "")
+
+
+@pytest.mark.parametrize("label", [False, True])
+def test_native_reader_matches_reference_semantics(label, tmp_path):
+    """Fuzz of the grammar (quoting, blank lines, \\r / \\r\\n records, '_'
+    separators, exponents, inf/nan spellings, Unicode digits and blanks, ragged
+    rows) against the csv-module restatement of the reference readers."""
+    rng = np.random.default_rng(11 + label)
+    p = tmp_path / "f.csv"
+    for case in range(400):
+        text = _fuzz_text(rng, label)
+        p.write_bytes(text.encode("utf-8"))
+        oracle = O.read_skill_matrix_rows if label else O.load_csv_rows
+        try:
+            want = oracle(p)
+            err = None
+        except (O.CsvOracleError, O.OracleError, IndexError) as exc:
+            want, err = None, (type(exc), str(exc))
+        kinds = {P.CsvFormatError: O.CsvOracleError, P.ParameterError: O.OracleError, IndexError: IndexError}
+        try:
+            got = P.read_skill_matrix(p) if label else P.load_csv(p)
+            gerr = None
+        except tuple(kinds) as exc:
+            got, gerr = None, (next(v for k, v in kinds.items() if isinstance(exc, k)), str(exc))
+        assert gerr == err, (case, repr(text))
+        if err is None:
+            if label:
+                assert got.names == want[0]
+                assert np.array_equal(np.isnan(got.rho), np.isnan(want[1]))
+                assert np.array_equal(np.nan_to_num(got.rho), np.nan_to_num(want[1])), (case, repr(text))
+            else:
+                assert got.names == want[0]
+                vals = np.array([s.values for s in got]).T
+                assert vals.tobytes() == np.array(want[1], dtype=np.float64).reshape(vals.shape).tobytes(), repr(text)
 
 
 def test_npz_round_trip(tmp_path):
