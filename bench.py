@@ -328,28 +328,41 @@ def run_ours(args):
 
     import paper_2105_12301_b200 as P
     from paper_2105_12301_b200 import _native as nat
-    from paper_2105_12301_b200.distributed import all_gather_rows, broadcast_, shard_bounds, xmap_sharded
+    from paper_2105_12301_b200.distributed import (all_gather_rows, broadcast_, init_native_comm, shard_bounds,
+                                                   xmap_native_rank, xmap_sharded)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    # one process per GPU; CMB_DIST_BACKEND=gloo lets ranks share a GPU (functional runs)
-    backend = os.environ.get("CMB_DIST_BACKEND", "nccl")
+    # one process per GPU.  N > 1 data path: libcmb200's own NCCL communicator
+    # (cmb_xmap_rank: broadcast X, library shard, grouped send/recv gather to
+    # rank 0); torch.distributed (gloo, CPU) is plumbing only: the id exchange,
+    # barriers, the max over ranks.  CMB_DIST_BACKEND=gloo: the older torch path
+    # with ranks sharing one GPU (functional runs without NCCL).
+    backend = os.environ.get("CMB_DIST_BACKEND", "native")
+    # CMB_FORCE_NATIVE=1 runs the native rank path at N = 1 too (a one-rank
+    # communicator: how the N > 1 path is exercised on a one-GPU box)
+    native = (world > 1 and backend != "gloo") or os.environ.get("CMB_FORCE_NATIVE") == "1"
     local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     os.environ["CMB_DEVICE"] = str(local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+    comm_info = None
+    if world > 1 or native:
+        if native:
+            os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator lines (nranks) on stderr
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        dist.init_process_group("gloo")
+        if native:
+            comm_info = init_native_comm(local)
     dev = torch.device("cuda", local)
     N, T = args.n, args.t
 
-    # ---- setup (untimed): data on rank 0, E* from device edim
-    X_host = make_data(N, T, args.seed) if rank == 0 else np.empty((N, T), np.float32)
+    # ---- setup (untimed): the seeded data (generated by every rank for its edim
+    #      shard; the timed step broadcasts rank 0's copy), E* from device edim
+    X_host = make_data(N, T, args.seed) if (rank == 0 or native) else np.empty((N, T), np.float32)
     Xd = torch.from_numpy(X_host).to(dev)
-    if world > 1:
+    if world > 1 and not native:
         broadcast_(Xd, src=0)
     rho_e = torch.empty((N, args.e_max), dtype=torch.float64, device=dev)
     est_d = torch.empty(N, dtype=torch.int32, device=dev)
@@ -361,24 +374,32 @@ def run_ours(args):
              rho_e[lo_s:].data_ptr(), est_d[lo_s:].data_ptr(), torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     t_edim = time.perf_counter() - t0
-    if world > 1:
-        est_d = all_gather_rows(est_d[lo_s:hi_s].contiguous(), N)
-    estar = est_d.cpu().numpy().astype(np.int32)
+    if dist.is_initialized():
+        parts = [None] * world
+        dist.all_gather_object(parts, est_d[lo_s:hi_s].cpu().numpy())
+        estar = np.concatenate(parts).astype(np.int32)
+    else:
+        estar = est_d.cpu().numpy().astype(np.int32)
+    near = P.near_ties(rho_e[lo_s:hi_s].cpu().numpy(), estar[lo_s:hi_s])
     valid = int(np.sum(estar > 0))
     hist = {int(e): int(c) for e, c in zip(*np.unique(estar, return_counts=True))}
 
     stats = np.zeros(8)
     lo, hi = shard_bounds(N, world, rank)
     n_sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    rho0 = torch.empty((N, N), dtype=torch.float32, device=dev) if (native and rank == 0) else None
 
     def step():
+        if native:
+            xmap_native_rank(Xd, estar, 1, rho0, stats, local, torch.cuda.current_stream().cuda_stream)
+            return rho0
         return xmap_sharded(Xd, estar, 1, stats=stats, broadcast=True)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     nat.diagnostics(local)
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
@@ -391,17 +412,12 @@ def run_ours(args):
             look_s.append(stats[1])
         e1.record(s)
         torch.cuda.synchronize()
-    if world > 1:
+    if dist.is_initialized():
         dist.barrier()
     ms = e0.elapsed_time(e1) / args.steps
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        if backend == "gloo":
-            th = t_max.cpu()
-            dist.all_reduce(th, op=dist.ReduceOp.MAX)
-            t_max = th
-        else:
-            dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_max = torch.tensor([ms], dtype=torch.float64)
+    if dist.is_initialized():
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms = float(t_max.item())
     diag = nat.diagnostics(local)
     pairs = float(valid) * float(valid)
@@ -459,7 +475,7 @@ def run_ours(args):
 
     # ---- e2e through the public C ABI with host buffers (rank 0 drives N = 1)
     e2e = None
-    if not args.no_e2e and world == 1:
+    if not args.no_e2e and world == 1 and not native:
         xp = torch.from_numpy(X_host).pin_memory()
         outp = torch.empty((N, N), dtype=torch.float32).pin_memory()
         st = np.zeros(8)
@@ -481,10 +497,41 @@ def run_ours(args):
                "ms_per_step": el * 1e3}
         del outp, xp
 
-    # ---- e2e at N > 1: X from pinned host memory on rank 0 (H2D), NCCL broadcast,
-    #      sharded cross map, every rank's rho slab copied to its pinned host buffer
-    #      (one PCIe link per GPU); wall time per step, max over ranks
-    if not args.no_e2e and world > 1:
+    # ---- e2e at N > 1 (native): X from pinned host memory on rank 0 (H2D), the
+    #      sharded cross map with its NCCL broadcast and gather, rho[lib, tgt]
+    #      (N x N fp32) from rank 0's device to pinned host memory; wall time per
+    #      step, max over ranks
+    if not args.no_e2e and native:
+        xp = torch.from_numpy(X_host).pin_memory() if rank == 0 else None
+        hp = torch.empty((N, N), dtype=torch.float32).pin_memory() if rank == 0 else None
+
+        def e2e_step():
+            if rank == 0:
+                Xd.copy_(xp, non_blocking=True)
+            step()
+            if rank == 0:
+                hp.copy_(rho0, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+
+        for _ in range(max(1, args.warmup - 2)):
+            e2e_step()
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e2e_step()
+        el = (time.perf_counter() - t0) / args.steps
+        dist.barrier()
+        el_t = torch.tensor([el], dtype=torch.float64)
+        dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
+        el = float(el_t.item())
+        e2e = {"value": pairs / el, "unit": UNIT, "h2d_bytes_per_step": int(N * T * 4),
+               "d2h_bytes_per_step": int(N * N * 4), "layout": "library-major rho on rank 0 (gathered over NCCL)",
+               "ms_per_step": el * 1e3}
+        del xp, hp
+
+    # ---- e2e at N > 1 (torch / gloo functional mode): every rank's rho slab to
+    #      its pinned host buffer; wall time per step, max over ranks
+    if not args.no_e2e and world > 1 and not native:
         xp = torch.from_numpy(X_host).pin_memory() if rank == 0 else None
         Xe = torch.empty((N, T), dtype=torch.float32, device=dev)
         host = {}
@@ -508,12 +555,7 @@ def run_ours(args):
         el = (time.perf_counter() - t0) / args.steps
         dist.barrier()
         el_t = torch.tensor([el], dtype=torch.float64)
-        if backend == "gloo":
-            dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
-        else:
-            el_d = el_t.to(dev)
-            dist.all_reduce(el_d, op=dist.ReduceOp.MAX)
-            el_t = el_d.cpu()
+        dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
         el = float(el_t.item())
         d2h = int(host["slab"].numel() * 4) * world
         e2e = {"value": pairs / el, "unit": UNIT, "h2d_bytes_per_step": int(N * T * 4),
@@ -524,7 +566,7 @@ def run_ours(args):
     # ---- CPU baseline (the stock reference path on the host cores) on whole
     #      library rows, which double as the parity check of this run's rho
     cpu = parity = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    if rank == 0 and world == 1 and not args.no_cpu and not native:
         v, sample, el, libs, rows, kind = cpu_sample(X_host, estar, args.cpu_seconds, seed=args.seed, min_rows=3)
         cpu = {"value": v, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": kind, "sample": sample}
         got = rho_last[:N, libs].T.cpu().numpy().astype(np.float64)  # slab column = library
@@ -545,7 +587,11 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "fp32 (fp64 selection + skill)", "data": "synthetic",
             "config": workload_config(args, valid, estar),
-            "parallelism": f"library rows x{world}",
+            "parallelism": f"library rows x{world}" + (" (libcmb200 NCCL: broadcast X, gather rho rows)"
+                                                         if native else ""),
+            "nccl": comm_info,
+            "edim_near_ties": {"tol": 1e-4, "count_rank0_shard": len(near),
+                               "min_gap": min((d["gap"] for d in near), default=None)},
             "parity": parity, "estar_equals_fixture": estar_check,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
@@ -564,7 +610,7 @@ def run_ours(args):
                       "exact_fallback_rows": diag["exact_fallback_rows"], "rows_checked": diag["rows_checked"]},
         }
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 

@@ -118,6 +118,34 @@ int cmb_xmap_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld
                  const int32_t* estar, int tau, int64_t lib_begin, int64_t lib_end,
                  float* rhoT_dev, int64_t ldr, void* stream, double* stats_out);
 
+/* ---- multi-GPU cross map (shards ccm.py:131-149 by library) -- */
+/* NCCL is loaded at run time (libnccl.so.2); without it these return CMB_ERR_NCCL.
+ * Every rank computes the rho rows of its contiguous library block [lo, hi)
+ * (sizes differ by at most one) for all targets; the only collectives are the
+ * broadcast of X from rank 0 and the gather of the library-major row blocks
+ * to rank 0 (grouped ncclSend / ncclRecv).  rho is bitwise identical for any
+ * rank count.  stats_out (nullable, 8 doubles): tables, lookup, total seconds,
+ * tables_built, distinct_E, pairs, fixup items, broadcast + gather seconds.   */
+
+/* 128-byte ncclUniqueId for a one-process-per-GPU job (rank 0 creates it and
+ * hands it to the others, e.g. over torch.distributed's store).             */
+int cmb_nccl_unique_id(void* id_out);
+/* Communicator of this process's device `dev` as rank `rank` of `nranks`.    */
+int cmb_nccl_init_rank(int dev, const void* id, int nranks, int rank);
+/* Ranks in the communicator of `dev`, this process's rank, NCCL version.     */
+int cmb_nccl_info(int dev, int* nranks, int* rank, int* version);
+int cmb_nccl_destroy(int dev);
+/* One rank of the sharded cross map: X_dev[N][len] float32 on `dev`, valid on
+ * rank 0 (broadcast in place); estar[N] host on every rank; rank 0 receives
+ * rho_dev[lib * N + tgt] (library-major, device, N x N), other ranks pass NULL.
+ * `stream` (cudaStream_t, NULL = the library's); returns when done.          */
+int cmb_xmap_rank(int dev, float* X_dev, int64_t N, int64_t len, const int32_t* estar, int tau,
+                  float* rho_dev, void* stream, double* stats_out);
+/* The same job from one process: devs[0..ndev) (ncclCommInitAll, one host
+ * thread per device), host X[N][len] float32, host rho_out[lib * N + tgt].   */
+int cmb_xmap_multi(const int* devs, int ndev, const float* X, int64_t N, int64_t len,
+                   const int32_t* estar, int tau, float* rho_out, double* stats_out);
+
 /* Device-resident edim: X_dev[N][ld] float32; rho_dev[N][E_max] float64,
  * estar_dev[N] int32.                                                       */
 int cmb_edim_dev(int dev, const float* X_dev, int64_t N, int64_t len, int64_t ld, int E_max,

@@ -44,6 +44,12 @@ _SIGNATURES = {
     "cmb_xmap64": ([C.c_int, _P, _i64, _i64, _P, C.c_int, _P, C.c_int, _P], C.c_int),
     "cmb_xmap_dev": ([C.c_int, _P, _i64, _i64, _i64, _P, C.c_int, _i64, _i64, _P, _i64, _P, _P],
                      C.c_int),
+    "cmb_nccl_unique_id": ([_P], C.c_int),
+    "cmb_nccl_init_rank": ([C.c_int, _P, C.c_int, C.c_int], C.c_int),
+    "cmb_nccl_info": ([C.c_int, _P, _P, _P], C.c_int),
+    "cmb_nccl_destroy": ([C.c_int], C.c_int),
+    "cmb_xmap_rank": ([C.c_int, _P, _i64, _i64, _P, C.c_int, _P, _P, _P], C.c_int),
+    "cmb_xmap_multi": ([_P, C.c_int, _P, _i64, _i64, _P, C.c_int, _P, _P], C.c_int),
     "cmb_edim_dev": ([C.c_int, _P, _i64, _i64, _i64, C.c_int, C.c_int, C.c_int, _P, _P, _P],
                      C.c_int),
     "cmb_ccm_convergence": ([C.c_int, _P, _i64, _i64, C.c_int, C.c_int, _P, _P, _i64, _P, C.c_int,

@@ -3,7 +3,11 @@
 #include "cmb_common.cuh"
 #include "kernels.cuh"
 
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <algorithm>
+#include <thread>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -62,7 +66,7 @@ struct DevBuf {
 enum BufId {
   B_X64, B_X32, B_ERR, B_MEAN, B_Y, B_SLOT_TGT, B_SLOT_E, B_OBS_S, B_OBS_SS, B_OBS_C, B_LIBROWS,
   B_LIBCOL, B_TAB, B_COUNTER, B_RHOT, B_RHO, B_PART, B_LAST, B_LMEAN, B_A, B_B, B_C, B_D, B_E,
-  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_YH, B_FIX, B_NBUF
+  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_YH, B_FIX, B_SLAB, B_NBUF
 };
 
 // page-locked host buffer (the pageable-output bounce slabs of xmap_host)
@@ -105,6 +109,8 @@ struct Ctx {
   std::mutex mu;
   DevBuf buf[B_NBUF];
   HostBuf bounce[2];
+  ncclComm_t comm = nullptr;  // cmb_nccl_init_rank / cmb_xmap_multi
+  int nranks = 1, rank = 0;
   bool ready = false;
 };
 
@@ -504,6 +510,8 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   return CMB_OK;
 }
 
+static void nccl_destroy(ncclComm_t c);  // NCCL section below
+
 }  // namespace cmb
 
 using namespace cmb;
@@ -540,6 +548,8 @@ int cmb_shutdown(void) {
     cudaSetDevice(c->dev);
     for (auto& b : c->buf) b.release();
     for (auto& b : c->bounce) b.release();
+    if (c->comm) nccl_destroy(c->comm);
+    c->comm = nullptr;
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     c->stream = nullptr;
@@ -896,6 +906,281 @@ int cmb_xmap64(int dev, const double* X, int64_t N, int64_t len, const int32_t* 
   CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
   CMB_CTX(dev);
   return xmap_host(ctx, st, X, true, N, len, estar, tau, rho_out, layout, stats_out);
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- NCCL (multi-GPU)
+// NCCL is resolved at run time (dlopen "libnccl.so.2": the copy PyTorch already
+// loaded when there is one, else the system's), so the library has no link-time
+// NCCL dependency and never mixes two NCCL versions in one process.
+namespace cmb {
+
+struct NcclApi {
+  bool tried = false, ok = false;
+  std::string why;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclCommInitAll) commInitAll = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclCommCount) commCount = nullptr;
+  decltype(&ncclBroadcast) broadcast = nullptr;
+  decltype(&ncclSend) send = nullptr;
+  decltype(&ncclRecv) recv = nullptr;
+  decltype(&ncclGroupStart) groupStart = nullptr;
+  decltype(&ncclGroupEnd) groupEnd = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+  decltype(&ncclGetVersion) getVersion = nullptr;
+};
+
+static std::mutex g_nccl_mu;
+static NcclApi g_nccl;
+
+static NcclApi* nccl_api() {
+  std::lock_guard<std::mutex> g(g_nccl_mu);
+  if (!g_nccl.tried) {
+    g_nccl.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      g_nccl.why = dlerror() ? dlerror() : "libnccl.so.2 not found";
+    } else {
+      bool all = true;
+      auto sym = [&](auto& fp, const char* name) {
+        fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+        if (!fp) all = false;
+      };
+      sym(g_nccl.getUniqueId, "ncclGetUniqueId");
+      sym(g_nccl.commInitRank, "ncclCommInitRank");
+      sym(g_nccl.commInitAll, "ncclCommInitAll");
+      sym(g_nccl.commDestroy, "ncclCommDestroy");
+      sym(g_nccl.commCount, "ncclCommCount");
+      sym(g_nccl.broadcast, "ncclBroadcast");
+      sym(g_nccl.send, "ncclSend");
+      sym(g_nccl.recv, "ncclRecv");
+      sym(g_nccl.groupStart, "ncclGroupStart");
+      sym(g_nccl.groupEnd, "ncclGroupEnd");
+      sym(g_nccl.errorString, "ncclGetErrorString");
+      sym(g_nccl.getVersion, "ncclGetVersion");
+      g_nccl.ok = all;
+      if (!all) g_nccl.why = "libnccl.so.2 lacks a required symbol";
+    }
+  }
+  return &g_nccl;
+}
+
+static void nccl_destroy(ncclComm_t c) {
+  if (nccl_api()->ok) nccl_api()->commDestroy(c);
+}
+
+#define CMB_NCCL(call)                                                                        \
+  do {                                                                                        \
+    ncclResult_t _r = (call);                                                                 \
+    if (_r != ncclSuccess) {                                                                  \
+      ::cmb::set_error("NCCL error %d (%s) in %s", (int)_r, nccl_api()->errorString(_r), #call); \
+      return CMB_ERR_NCCL;                                                                    \
+    }                                                                                         \
+  } while (0)
+
+static int need_nccl() {
+  NcclApi* api = nccl_api();
+  if (!api->ok) {
+    set_error("NCCL unavailable: %s", api->why.c_str());
+    return CMB_ERR_NCCL;
+  }
+  return CMB_OK;
+}
+
+// contiguous library block of rank r (sizes differ by at most one; distributed.py shard_bounds)
+static void shard_bounds(int64_t n, int world, int r, int64_t* lo, int64_t* hi) {
+  const int64_t base = n / world, extra = n % world;
+  *lo = r * base + std::min<int64_t>(r, extra);
+  *hi = *lo + base + (r < extra ? 1 : 0);
+}
+
+// One rank's part of the sharded cross map (the caller holds ctx->mu, device set):
+// broadcast X from rank 0, rho of libraries [lo, hi) for every target
+// (xmap_core), the shard transposed to library-major rows, and the rows gathered
+// to rank 0 into rho_lm[N][N] (library-major, device, rank 0 only) with grouped
+// send/recv.  Per-pair arithmetic does not depend on the rank count, so rho is
+// bitwise identical for any G.  stats: {tables, lookup, total, tables_built,
+// distinct_E, pairs, fixups, broadcast + gather seconds}.
+static int xmap_rank_core(Ctx* ctx, cudaStream_t st, float* X_dev, int64_t N, int64_t len,
+                          const int32_t* estar, int tau, float* rho_lm, double* stats_out) {
+  NcclApi* api = nccl_api();
+  const int G = ctx->nranks, r = ctx->rank;
+  EventSet evs;
+  cudaEvent_t e0, e1, e2, e3;
+  CMB_CUDA(evs.make(&e0, 0));
+  CMB_CUDA(evs.make(&e1, 0));
+  CMB_CUDA(evs.make(&e2, 0));
+  CMB_CUDA(evs.make(&e3, 0));
+  CMB_CUDA(cudaEventRecord(e0, st));
+  CMB_NCCL(api->broadcast(X_dev, X_dev, (size_t)(N * len), ncclFloat, 0, ctx->comm, st));
+  CMB_CUDA(cudaEventRecord(e1, st));
+  int64_t lo, hi;
+  shard_bounds(N, G, r, &lo, &hi);
+  const int64_t w = hi - lo, ldr = std::max<int64_t>(4, (w + 3) / 4 * 4);
+  CMB_CUDA(ctx->buf[B_RHOT].ensure(sizeof(float) * (size_t)N * ldr + 16));
+  XmapStats s;
+  CMB_TRY(xmap_core(ctx, st, X_dev, N, len, len, estar, tau, lo, hi, ctx->buf[B_RHOT].as<float>(), ldr, &s));
+  CMB_CUDA(cudaEventRecord(e2, st));
+  // library-major rows of the shard: straight into the result on rank 0
+  float* mine = rho_lm;
+  if (r != 0) {
+    CMB_CUDA(ctx->buf[B_SLAB].ensure(sizeof(float) * (size_t)std::max<int64_t>(w, 1) * N));
+    mine = ctx->buf[B_SLAB].as<float>();
+  }
+  if (w > 0)
+    CMB_CUDA(launch_transpose_f32(ctx->buf[B_RHOT].as<float>(), N, w, ldr, r == 0 ? mine + lo * N : mine, N, st));
+  CMB_NCCL(api->groupStart());
+  if (r == 0) {
+    for (int g = 1; g < G; ++g) {
+      int64_t glo, ghi;
+      shard_bounds(N, G, g, &glo, &ghi);
+      if (ghi > glo) CMB_NCCL(api->recv(rho_lm + glo * N, (size_t)((ghi - glo) * N), ncclFloat, g, ctx->comm, st));
+    }
+  } else if (w > 0) {
+    CMB_NCCL(api->send(mine, (size_t)(w * N), ncclFloat, 0, ctx->comm, st));
+  }
+  CMB_NCCL(api->groupEnd());
+  CMB_CUDA(cudaEventRecord(e3, st));
+  CMB_CUDA(cudaEventSynchronize(e3));
+  float ms_b = 0, ms_g = 0, ms_t = 0;
+  cudaEventElapsedTime(&ms_b, e0, e1);
+  cudaEventElapsedTime(&ms_g, e2, e3);
+  cudaEventElapsedTime(&ms_t, e0, e3);
+  if (stats_out) {
+    const double v[8] = {s.t_tables, s.t_lookup, ms_t * 1e-3, s.tables, s.distinct, s.pairs, s.fixups,
+                         (ms_b + ms_g) * 1e-3};
+    memcpy(stats_out, v, sizeof(v));
+  }
+  return CMB_OK;
+}
+
+}  // namespace cmb
+
+extern "C" {
+
+int cmb_nccl_unique_id(void* id_out) {
+  CMB_TRY(need_nccl());
+  ncclUniqueId id;
+  CMB_NCCL(nccl_api()->getUniqueId(&id));
+  memcpy(id_out, &id, sizeof(id));
+  return CMB_OK;
+}
+
+int cmb_nccl_init_rank(int dev, const void* id, int nranks, int rank) {
+  CMB_PARAM(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank %d of %d", rank, nranks);
+  CMB_TRY(need_nccl());
+  CMB_CTX(dev);
+  (void)st;
+  NcclApi* api = nccl_api();
+  if (ctx->comm) {
+    api->commDestroy(ctx->comm);
+    ctx->comm = nullptr;
+  }
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  CMB_NCCL(api->commInitRank(&ctx->comm, nranks, uid, rank));
+  ctx->nranks = nranks;
+  ctx->rank = rank;
+  return CMB_OK;
+}
+
+int cmb_nccl_info(int dev, int* nranks, int* rank, int* version) {
+  CMB_TRY(need_nccl());
+  CMB_CTX(dev);
+  (void)st;
+  CMB_PARAM(ctx->comm != nullptr, "device %d has no NCCL communicator", dev);
+  CMB_NCCL(nccl_api()->commCount(ctx->comm, nranks));
+  *rank = ctx->rank;
+  CMB_NCCL(nccl_api()->getVersion(version));
+  return CMB_OK;
+}
+
+int cmb_nccl_destroy(int dev) {
+  CMB_CTX(dev);
+  (void)st;
+  if (ctx->comm) nccl_api()->commDestroy(ctx->comm);
+  ctx->comm = nullptr;
+  ctx->nranks = 1;
+  ctx->rank = 0;
+  return CMB_OK;
+}
+
+int cmb_xmap_rank(int dev, float* X_dev, int64_t N, int64_t len, const int32_t* estar, int tau, float* rho_dev,
+                  void* stream, double* stats_out) {
+  CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
+  CMB_TRY(need_nccl());
+  CMB_CTX(dev);
+  CMB_PARAM(ctx->comm != nullptr, "device %d has no NCCL communicator (cmb_nccl_init_rank)", dev);
+  CMB_PARAM(ctx->rank != 0 || rho_dev != nullptr, "rank 0 needs the result buffer");
+  cudaStream_t use = stream ? reinterpret_cast<cudaStream_t>(stream) : st;
+  return xmap_rank_core(ctx, use, X_dev, N, len, estar, tau, rho_dev, stats_out);
+}
+
+int cmb_xmap_multi(const int* devs, int ndev, const float* X, int64_t N, int64_t len, const int32_t* estar,
+                   int tau, float* rho_out, double* stats_out) {
+  CMB_PARAM(ndev >= 1 && devs, "no devices");
+  CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
+  CMB_TRY(need_nccl());
+  NcclApi* api = nccl_api();
+  std::vector<Ctx*> ctxs(ndev);
+  for (int g = 0; g < ndev; ++g) CMB_TRY(get_ctx(devs[g], &ctxs[g]));
+  std::vector<ncclComm_t> comms(ndev);
+  CMB_NCCL(api->commInitAll(comms.data(), ndev, devs));
+  std::vector<int> rc(ndev, CMB_OK);
+  std::vector<std::string> msg(ndev);
+  std::vector<double> st0(8, 0.0);
+  // one host thread per device, each the rank body of a one-process-per-GPU job
+  auto body = [&](int g) {
+    Ctx* ctx = ctxs[g];
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    int r = CMB_OK;
+    do {
+      if (cudaSetDevice(ctx->dev) != cudaSuccess) { r = cuda_fail(cudaGetLastError(), "cudaSetDevice", __FILE__, __LINE__); break; }
+      ncclComm_t keep = ctx->comm;
+      const int keep_n = ctx->nranks, keep_r = ctx->rank;
+      ctx->comm = comms[g];
+      ctx->nranks = ndev;
+      ctx->rank = g;
+      float* rho_full = nullptr;
+      if (ctx->buf[B_X32].ensure(sizeof(float) * N * len + 256) != cudaSuccess ||
+          (g == 0 && ctx->buf[B_RHO].ensure(sizeof(float) * (size_t)N * N) != cudaSuccess)) {
+        set_error("out of device memory for the sharded cross map");
+        r = CMB_ERR_CUDA;
+      } else {
+        if (g == 0) {
+          rho_full = ctx->buf[B_RHO].as<float>();
+          if (cudaMemcpyAsync(ctx->buf[B_X32].p, X, sizeof(float) * N * len, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess)
+            r = cuda_fail(cudaGetLastError(), "H2D X", __FILE__, __LINE__);
+        }
+        if (r == CMB_OK)
+          r = xmap_rank_core(ctx, ctx->stream, ctx->buf[B_X32].as<float>(), N, len, estar, tau, rho_full,
+                             g == 0 ? st0.data() : nullptr);
+        if (r == CMB_OK && g == 0 &&
+            cudaMemcpy(rho_out, rho_full, sizeof(float) * (size_t)N * N, cudaMemcpyDeviceToHost) != cudaSuccess)
+          r = cuda_fail(cudaGetLastError(), "D2H rho", __FILE__, __LINE__);
+      }
+      ctx->comm = keep;
+      ctx->nranks = keep_n;
+      ctx->rank = keep_r;
+    } while (0);
+    rc[g] = r;
+    if (r) msg[g] = cmb_last_error();
+  };
+  std::vector<std::thread> th;
+  for (int g = 0; g < ndev; ++g) th.emplace_back(body, g);
+  for (auto& t : th) t.join();
+  for (auto c : comms) api->commDestroy(c);
+  for (int g = 0; g < ndev; ++g)
+    if (rc[g]) {
+      set_error("device %d: %s", devs[g], msg[g].c_str());
+      return rc[g];
+    }
+  if (stats_out) memcpy(stats_out, st0.data(), 8 * sizeof(double));
+  return CMB_OK;
 }
 
 int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E, int tau,

@@ -8,8 +8,18 @@ rank 0.  There is no other collective: pairs are independent and every rank
 processes the same distinct-E set, so per-rank work is uniform and rho is
 bitwise identical for any G (per-pair arithmetic does not depend on G).
 
-torch.distributed is plumbing only (process group, device buffers, the two
-collectives); all arithmetic runs in libcmb200.
+Two implementations of the same plan:
+
+* ``init_native_comm`` + ``xmap_native_rank`` -- the product path: libcmb200's
+  own NCCL communicator (``cmb_nccl_init_rank``; the 128-byte id travels over
+  torch.distributed's CPU group, which is only plumbing) and
+  ``cmb_xmap_rank``, which broadcasts X, computes the rank's library block and
+  gathers the library-major rows to rank 0 with grouped ncclSend/ncclRecv --
+  no torch collective on the data path, rank 0 holds rho plus one shard.
+* ``xmap_sharded`` -- the same plan over torch.distributed collectives, kept
+  for gloo runs (ranks sharing one GPU, CPU tests with an oracle ``compute``).
+
+All arithmetic runs in libcmb200.
 """
 
 from __future__ import annotations
@@ -133,3 +143,51 @@ def assemble(rhoT_slabs, n: int, world: int) -> np.ndarray:
         lo, hi = shard_bounds(n, world, g)
         cols.append(rt[:, g * w: g * w + (hi - lo)])
     return np.concatenate(cols, axis=1).T
+
+
+# ---------------------------------------------------------------- native NCCL path
+def init_native_comm(device: int, group=None) -> dict:
+    """Create this process's libcmb200 NCCL communicator (rank and size of the
+    torch.distributed group; one process per GPU).  Returns {"nranks", "rank",
+    "nccl_version"} as reported by the communicator itself."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    uid = np.zeros(128, dtype=np.uint8)
+    if rank == 0:
+        nat.call("cmb_nccl_unique_id", nat.ptr(uid))
+    box = [uid.tobytes() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    uid = np.frombuffer(box[0], dtype=np.uint8).copy()
+    nat.call("cmb_nccl_init_rank", device, nat.ptr(uid), world, rank)
+    n, r, v = (np.zeros(1, dtype=np.int32) for _ in range(3))
+    nat.call("cmb_nccl_info", device, nat.ptr(n), nat.ptr(r), nat.ptr(v))
+    return {"nranks": int(n[0]), "rank": int(r[0]), "nccl_version": int(v[0])}
+
+
+def xmap_native_rank(X, estar: np.ndarray, tau: int, rho=None, stats: np.ndarray | None = None,
+                     device: int | None = None, stream_handle: int | None = None) -> None:
+    """One rank of the sharded cross map through libcmb200 (cmb_xmap_rank).
+
+    ``X``: torch float32 [N][T] on this rank's device (valid on rank 0; the
+    broadcast overwrites it elsewhere).  ``rho``: on rank 0 a torch float32
+    [N][N] device buffer that receives rho[lib, tgt]; None on other ranks."""
+    N, T = X.shape
+    assert X.is_contiguous() and (rho is None or rho.is_contiguous())
+    est = np.ascontiguousarray(estar, dtype=np.int32)
+    dev = X.device.index if device is None else device
+    nat.call("cmb_xmap_rank", dev, X.data_ptr(), N, T, nat.ptr(est), tau,
+             None if rho is None else rho.data_ptr(), stream_handle, nat.ptr(stats))
+
+
+def xmap_multi(values: np.ndarray, estar, devices, tau: int = 1) -> np.ndarray:
+    """Single-process multi-device cross map (cmb_xmap_multi): ``values`` (series,
+    time) float32 host array; returns rho[lib, tgt] float32."""
+    X = np.ascontiguousarray(values, dtype=np.float32)
+    N, T = X.shape
+    est = np.ascontiguousarray(estar, dtype=np.int32)
+    devs = np.ascontiguousarray(devices, dtype=np.int32)
+    out = np.empty((N, N), dtype=np.float32)
+    st = np.zeros(8)
+    nat.call("cmb_xmap_multi", nat.ptr(devs), devs.size, nat.ptr(X), N, T, nat.ptr(est), tau, nat.ptr(out),
+             nat.ptr(st))
+    return out

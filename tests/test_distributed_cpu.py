@@ -94,3 +94,40 @@ def test_uneven_all_gather_and_broadcast(n):
     mp.spawn(_gather_worker, args=(3, _free_port(), n, out), nprocs=3, join=True)
     assert out[:n].tolist() == [3.0 * i for i in range(n)]
     assert out[n:].tolist() == [0.0, 1.0, 2.0, 3.0, 4.0]
+
+
+def _comm_worker(rank, world, port, out):
+    """init_native_comm's plumbing with libcmb200's entry points replaced by a
+    recorder: rank 0's 128-byte id must reach every rank's cmb_nccl_init_rank."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2105_12301_b200 import distributed as D
+    seen = {}
+
+    def fake_call(name, *args):
+        if name == "cmb_nccl_unique_id":
+            arr = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint8 * 128).from_address(args[0]))
+            arr[:] = np.arange(128, dtype=np.uint8) + 7
+        elif name == "cmb_nccl_init_rank":
+            dev, uid_ptr, nranks, r = args
+            uid = np.ctypeslib.as_array((np.ctypeslib.ctypes.c_uint8 * 128).from_address(uid_ptr)).copy()
+            seen.update(dev=dev, uid=uid, nranks=nranks, rank=r)
+        elif name == "cmb_nccl_info":
+            for ptr, v in zip(args[1:], (seen["nranks"], seen["rank"], 22809)):
+                np.ctypeslib.as_array((np.ctypeslib.ctypes.c_int32 * 1).from_address(ptr))[0] = v
+
+    D.nat.call = fake_call
+    info = D.init_native_comm(3)
+    ok = (info == {"nranks": world, "rank": rank, "nccl_version": 22809} and seen["dev"] == 3 and
+          np.array_equal(seen["uid"], np.arange(128, dtype=np.uint8) + 7))
+    out[rank] = 1.0 if ok else 0.0
+    dist.destroy_process_group()
+
+
+def test_native_comm_id_exchange():
+    """The libcmb200 NCCL communicator of the N > 1 bench path is created from one
+    id that rank 0 draws and torch.distributed (gloo, CPU) hands to the others."""
+    out = torch.zeros(3)
+    out.share_memory_()
+    mp.spawn(_comm_worker, args=(3, _free_port(), out), nprocs=3, join=True)
+    assert out.tolist() == [1.0, 1.0, 1.0]

@@ -97,3 +97,30 @@ def test_xmap_float64_offset_inputs():
         ref, _ = O.xmap([X[0], X[1]], est, 1, workers=1)
         assert np.array_equal(np.isnan(r), np.isnan(ref)), off
         assert np.nanmax(np.abs(r - ref)) <= RHO_TOL, (off, r, ref)
+
+
+def test_native_nccl_rank_path_single_rank():
+    """libcmb200's NCCL path (cmb_nccl_init_rank + cmb_xmap_rank, and the
+    single-process cmb_xmap_multi) with one rank on the one GPU of the test box:
+    broadcast, library shard and gather run for real and rho is bitwise equal to
+    the single-device cross map (the rank count never changes per-pair
+    arithmetic).  Multi-rank plumbing: tests/test_distributed_cpu.py."""
+    import torch
+    from paper_2105_12301_b200 import _native as nat
+    from paper_2105_12301_b200.distributed import xmap_multi, xmap_native_rank
+    X = P.mixed_dataset(300, 700, seed=5, dtype=np.float32)
+    est = np.array([(1, 2, 4, 7)[i % 4] for i in range(300)], dtype=np.int32)
+    ref = P.xmap(X.T, est, dtype=np.float32)
+    uid = np.zeros(128, dtype=np.uint8)
+    nat.call("cmb_nccl_unique_id", nat.ptr(uid))
+    nat.call("cmb_nccl_init_rank", 0, nat.ptr(uid), 1, 0)
+    n, r, v = (np.zeros(1, dtype=np.int32) for _ in range(3))
+    nat.call("cmb_nccl_info", 0, nat.ptr(n), nat.ptr(r), nat.ptr(v))
+    assert (int(n[0]), int(r[0])) == (1, 0) and int(v[0]) >= 22000
+    Xd = torch.from_numpy(X).cuda()
+    rho = torch.empty((300, 300), dtype=torch.float32, device="cuda")
+    st = np.zeros(8)
+    xmap_native_rank(Xd, est, 1, rho, st, 0, torch.cuda.current_stream().cuda_stream)
+    assert np.array_equal(rho.cpu().numpy(), ref, equal_nan=True)
+    nat.call("cmb_nccl_destroy", 0)
+    assert np.array_equal(xmap_multi(X, est, [0]), ref, equal_nan=True)
