@@ -109,6 +109,15 @@ int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* est
 int cmb_xmap64(int dev, const double* X, int64_t N, int64_t len, const int32_t* estar, int tau,
                float* rho_out, int layout, double* stats_out);
 
+/* cmb_xmap64 plus materialised predictions (lookup_batch(want_predictions=True)
+ * inside ccm_pairwise, prediction.py:145-153, ccm.py:148-149) for P caller-given
+ * (pair_lib[p], pair_tgt[p]) pairs, from the same tables and targets as rho:
+ * pred_out[p * len + t] for the n_E = len - (E*(tgt)-1)*tau embedded points,
+ * NaN after them and for pairs with an undefined series.                    */
+int cmb_xmap_predict(int dev, const double* X, int64_t N, int64_t len, const int32_t* estar, int tau,
+                     const int32_t* pair_lib, const int32_t* pair_tgt, int64_t P, float* rho_out, int layout,
+                     float* pred_out, double* stats_out);
+
 /* Device-resident shard of cmb_xmap for the multi-GPU driver: X_dev[N][ld]
  * (float32, on `dev`), libraries [lib_begin, lib_end); writes
  * rhoT_dev[tgt * ldr + (lib - lib_begin)] (target-major).  `stream` is a

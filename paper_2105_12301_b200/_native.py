@@ -42,6 +42,7 @@ _SIGNATURES = {
     "cmb_edim": ([C.c_int, _P, _i64, _i64, C.c_int, C.c_int, C.c_int, _P, _P], C.c_int),
     "cmb_xmap": ([C.c_int, _P, _i64, _i64, _P, C.c_int, _P, C.c_int, _P], C.c_int),
     "cmb_xmap64": ([C.c_int, _P, _i64, _i64, _P, C.c_int, _P, C.c_int, _P], C.c_int),
+    "cmb_xmap_predict": ([C.c_int, _P, _i64, _i64, _P, C.c_int, _P, _P, _i64, _P, C.c_int, _P, _P], C.c_int),
     "cmb_xmap_dev": ([C.c_int, _P, _i64, _i64, _i64, _P, C.c_int, _i64, _i64, _P, _i64, _P, _P],
                      C.c_int),
     "cmb_nccl_unique_id": ([_P], C.c_int),

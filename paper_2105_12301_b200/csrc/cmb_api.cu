@@ -66,7 +66,7 @@ struct DevBuf {
 enum BufId {
   B_X64, B_X32, B_ERR, B_MEAN, B_Y, B_SLOT_TGT, B_SLOT_E, B_OBS_S, B_OBS_SS, B_OBS_C, B_LIBROWS,
   B_LIBCOL, B_TAB, B_COUNTER, B_RHOT, B_RHO, B_PART, B_LAST, B_LMEAN, B_A, B_B, B_C, B_D, B_E,
-  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_YH, B_FIX, B_SLAB, B_NBUF
+  B_DIAG, B_EST, B_FMT_RHO, B_FMT_NAMES, B_FMT_OFF, B_FMT_LEN, B_FMT_ROWOFF, B_FMT_OUT, B_YH, B_FIX, B_SLAB, B_MU, B_PAIRS, B_SHIFT, B_PRED, B_NBUF
 };
 
 // page-locked host buffer (the pageable-output bounce slabs of xmap_host)
@@ -274,13 +274,26 @@ constexpr int kFixCap = 1 << 22;
 // that point (the host-buffer entry point overlaps its D2H copy with later chunks)
 using ChunkFn = std::function<int(int64_t, int64_t)>;
 
+// Materialised predictions requested with a cross map: pairs (lib[p], tgt[p]),
+// p < P, into pred_dev[p][ldp] (NaN past n_E and for undefined pairs); mu: per
+// series the fp64 mean removed before the fp32 sweep (cmb_xmap64), or null.
+struct PredReq {
+  const int32_t* lib = nullptr;
+  const int32_t* tgt = nullptr;
+  int64_t P = 0;
+  float* pred_dev = nullptr;
+  int64_t ldp = 0;
+  const double* mu = nullptr;
+};
+
 // X: float32 samples [N][ld] on the device.  x64_in (nullable): the caller's
 // float64 series [N][ld] when X was derived from them (cmb_xmap64: X centred,
 // err_in = per-series certification perturbation); otherwise X is promoted.
 static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64_t T, int64_t ld,
                      const int32_t* estar, int tau, int64_t lib_begin, int64_t lib_end, float* rhoT,
                      int64_t ldr, XmapStats* stats, const ChunkFn& on_chunk = nullptr,
-                     const double* x64_in = nullptr, const float* err_in = nullptr) {
+                     const double* x64_in = nullptr, const float* err_in = nullptr,
+                     const PredReq* preds = nullptr) {
   CMB_PARAM(tau >= 1, "tau must be >= 1, got %d", tau);
   CMB_PARAM(lib_begin >= 0 && lib_begin <= lib_end && lib_end <= N, "bad library range [%lld, %lld)",
             (long long)lib_begin, (long long)lib_end);
@@ -335,6 +348,24 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   }
   const int stage = lookup_stage_bytes((int)T, max_rec);
 
+  // ---- requested predictions: (library list index, target slot, E, output row),
+  //      sorted by library so each chunk's pairs are one contiguous range
+  std::vector<int4> pairs;
+  if (preds && preds->P > 0) {
+    std::vector<int> lib_index(N, -1), tgt_slot(N, -1);
+    for (size_t q = 0; q < lib_rows.size(); ++q) lib_index[lib_rows[q]] = (int)q;
+    for (size_t q = 0; q < slot_tgt.size(); ++q)
+      if (slot_tgt[q] >= 0) tgt_slot[slot_tgt[q]] = (int)q;
+    for (int64_t q = 0; q < preds->P; ++q) {
+      const int l = preds->lib[q], t = preds->tgt[q];
+      CMB_PARAM(l >= 0 && l < N && t >= 0 && t < N, "prediction pair %lld out of range", (long long)q);
+      if (lib_index[l] < 0 || tgt_slot[t] < 0) continue;  // undefined pair: its row stays NaN
+      pairs.push_back(make_int4(lib_index[l], tgt_slot[t], estar[t], (int)q));
+    }
+    std::stable_sort(pairs.begin(), pairs.end(), [](const int4& a, const int4& b) { return a.x < b.x; });
+    CMB_CUDA(launch_fill_nan(preds->pred_dev, preds->P, preds->ldp, preds->ldp, st));
+  }
+
   // ---- device staging
   const int64_t slots = (int64_t)slot_tgt.size();
   const int64_t ldy = slots;
@@ -370,6 +401,13 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     CMB_CUDA(launch_obs_moments(ctx->buf[B_Y].as<float>(), ldy, (int)T, tau, ctx->buf[B_SLOT_E].as<int32_t>(),
                                 slots, ctx->buf[B_OBS_S].as<double>(), ctx->buf[B_OBS_SS].as<double>(),
                                 ctx->buf[B_OBS_C].as<uint8_t>(), st));
+  }
+  if (!pairs.empty()) {
+    CMB_CUDA(ctx->buf[B_PAIRS].ensure(sizeof(int4) * pairs.size()));
+    CMB_CUDA(ctx->buf[B_SHIFT].ensure(sizeof(double) * slots));
+    CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_PAIRS].p, pairs.data(), sizeof(int4) * pairs.size(), cudaMemcpyHostToDevice, st));
+    CMB_CUDA(launch_slot_shift(ctx->buf[B_MEAN].as<double>(), preds->mu, ctx->buf[B_SLOT_TGT].as<int32_t>(), slots,
+                               ctx->buf[B_SHIFT].as<double>(), st));
   }
   const double* x64 = x64_in;
   if (!x64) {
@@ -469,6 +507,14 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->dev);
     CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(items, dev_sms), st));
     if (la.rot) CMB_CUDA(launch_lookup_fixup(la, st));
+    if (!pairs.empty()) {
+      const auto lo_it = std::lower_bound(pairs.begin(), pairs.end(), (int)c0,
+                                          [](const int4& a, int v) { return a.x < v; });
+      const auto hi_it = std::lower_bound(pairs.begin(), pairs.end(), (int)(c0 + nc),
+                                          [](const int4& a, int v) { return a.x < v; });
+      CMB_CUDA(launch_predict_pairs(la, ctx->buf[B_PAIRS].as<int4>() + (lo_it - pairs.begin()), hi_it - lo_it, c0,
+                                    ctx->buf[B_SHIFT].as<double>(), preds->pred_dev, preds->ldp, st));
+    }
     if (on_chunk) {
       // columns [first column of this chunk (0 for the first), first column of the next chunk)
       const int64_t col_lo = (c0 == 0) ? 0 : lib_rows[c0] - lib_begin;
@@ -790,7 +836,9 @@ namespace cmb {
 // bounce slabs (a device-to-pageable copy would block the host and serialise
 // the chunks).
 static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t N, int64_t len,
-                     const int32_t* estar, int tau, float* rho_out, int layout, double* stats_out) {
+                     const int32_t* estar, int tau, float* rho_out, int layout, double* stats_out,
+                     const int32_t* pair_lib = nullptr, const int32_t* pair_tgt = nullptr, int64_t P = 0,
+                     float* pred_out = nullptr) {
   const int64_t ldr = (N + 3) / 4 * 4;
   CMB_CUDA(ctx->buf[B_X32].ensure(sizeof(float) * N * len + 256));
   CMB_CUDA(ctx->buf[B_RHOT].ensure(sizeof(float) * N * ldr));
@@ -805,14 +853,27 @@ static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t
     CMB_CUDA(ctx->buf[B_X64].ensure(sizeof(double) * N * len));
     CMB_CUDA(ctx->buf[B_ERR].ensure(sizeof(float) * N));
     CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X64].p, X, sizeof(double) * N * len, cudaMemcpyHostToDevice, st));
+    CMB_CUDA(ctx->buf[B_MU].ensure(sizeof(double) * N));
     CMB_CUDA(launch_demote_center(ctx->buf[B_X64].as<double>(), N, len, ctx->buf[B_X32].as<float>(),
-                                  ctx->buf[B_ERR].as<float>(), st));
+                                  ctx->buf[B_ERR].as<float>(), ctx->buf[B_MU].as<double>(), st));
     x64 = ctx->buf[B_X64].as<double>();
     err = ctx->buf[B_ERR].as<float>();
   } else {
     CMB_CUDA(cudaMemcpyAsync(ctx->buf[B_X32].p, X, sizeof(float) * N * len, cudaMemcpyHostToDevice, st));
   }
   XmapStats s;
+  PredReq pr;
+  if (P > 0) {
+    pr.lib = pair_lib;
+    pr.tgt = pair_tgt;
+    pr.P = P;
+    pr.ldp = len;
+    CMB_CUDA(ctx->buf[B_PRED].ensure(sizeof(float) * (size_t)P * len));
+    pr.pred_dev = ctx->buf[B_PRED].as<float>();
+    CMB_CUDA(launch_fill_nan(pr.pred_dev, P, len, len, st));
+    pr.mu = f64 ? ctx->buf[B_MU].as<double>() : nullptr;
+  }
+  const PredReq* prp = P > 0 ? &pr : nullptr;
   if (layout == CMB_LAYOUT_TGT_MAJOR) {
     if (!ctx->copy_stream) CMB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
     cudaPointerAttributes attr;
@@ -861,7 +922,7 @@ static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t
       return CMB_OK;
     };
     const int rc = xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
-                             ctx->buf[B_RHOT].as<float>(), ldr, &s, on_chunk, x64, err);
+                             ctx->buf[B_RHOT].as<float>(), ldr, &s, on_chunk, x64, err, prp);
     cudaEvent_t copied;
     CMB_CUDA(evs.make(&copied, cudaEventDisableTiming));
     CMB_CUDA(cudaEventRecord(copied, ctx->copy_stream));
@@ -871,12 +932,14 @@ static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t
     CMB_TRY(drain());
   } else {
     CMB_TRY(xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
-                      ctx->buf[B_RHOT].as<float>(), ldr, &s, nullptr, x64, err));
+                      ctx->buf[B_RHOT].as<float>(), ldr, &s, nullptr, x64, err, prp));
     CMB_CUDA(ctx->buf[B_RHO].ensure(sizeof(float) * N * ldr));
     CMB_CUDA(launch_transpose_f32(ctx->buf[B_RHOT].as<float>(), N, N, ldr, ctx->buf[B_RHO].as<float>(), ldr, st));
     CMB_CUDA(cudaMemcpy2DAsync(rho_out, sizeof(float) * N, ctx->buf[B_RHO].p, sizeof(float) * ldr,
                                sizeof(float) * N, N, cudaMemcpyDeviceToHost, st));
   }
+  if (P > 0)
+    CMB_CUDA(cudaMemcpyAsync(pred_out, pr.pred_dev, sizeof(float) * (size_t)P * len, cudaMemcpyDeviceToHost, st));
   CMB_CUDA(cudaEventRecord(e1, st));
   CMB_CUDA(cudaEventSynchronize(e1));
   float ms = 0;
@@ -898,6 +961,16 @@ int cmb_xmap(int dev, const float* X, int64_t N, int64_t len, const int32_t* est
   CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
   CMB_CTX(dev);
   return xmap_host(ctx, st, X, false, N, len, estar, tau, rho_out, layout, stats_out);
+}
+
+int cmb_xmap_predict(int dev, const double* X, int64_t N, int64_t len, const int32_t* estar, int tau,
+                     const int32_t* pair_lib, const int32_t* pair_tgt, int64_t P, float* rho_out, int layout,
+                     float* pred_out, double* stats_out) {
+  CMB_PARAM(layout == CMB_LAYOUT_LIB_MAJOR || layout == CMB_LAYOUT_TGT_MAJOR, "bad layout %d", layout);
+  CMB_PARAM(N >= 1 && len >= 1, "empty dataset");
+  CMB_PARAM(P >= 0 && (P == 0 || (pair_lib && pair_tgt && pred_out)), "bad prediction pairs");
+  CMB_CTX(dev);
+  return xmap_host(ctx, st, X, true, N, len, estar, tau, rho_out, layout, stats_out, pair_lib, pair_tgt, P, pred_out);
 }
 
 int cmb_xmap64(int dev, const double* X, int64_t N, int64_t len, const int32_t* estar, int tau,

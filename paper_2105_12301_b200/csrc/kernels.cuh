@@ -90,6 +90,11 @@ constexpr int kLookupWarps = 16;
 constexpr int kNonResidentStage = 4096 + 16;
 int lookup_stage_bytes(int T, int max_rec_bytes);
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st);
+// predictions of (library, target) pairs from the chunk's tables: pairs[q] =
+// (library list index, target slot, E, output row), libraries [c0, c0 + nlib);
+// pred[row][t] = sum w y (centred fp32 targets) + shift[slot]
+cudaError_t launch_predict_pairs(const LookupArgs& a, const int4* pairs, int64_t npairs, int64_t c0,
+                                 const double* shift, float* pred, int64_t ldp, cudaStream_t st);
 // exact fp64 completion of the pairs the rotated lookup queued in a.fix
 cudaError_t launch_lookup_fixup(const LookupArgs& a, cudaStream_t st);
 
@@ -101,7 +106,10 @@ cudaError_t launch_promote(const float* x32, int64_t N, int64_t T, int64_t ld, d
 cudaError_t launch_demote(const double* x64, int64_t N, int64_t T, float* x32, float* err_m,
                           cudaStream_t st);
 cudaError_t launch_demote_center(const double* x64, int64_t N, int64_t T, float* x32, float* err_m,
-                                 cudaStream_t st);
+                                 double* mu, cudaStream_t st);
+// shift[slot] = mean[tgt] + (mu ? mu[tgt] : 0) of each slot's target (0 for padding)
+cudaError_t launch_slot_shift(const double* mean, const double* mu, const int32_t* slot_tgt, int64_t slots,
+                              double* shift, cudaStream_t st);
 cudaError_t launch_build_targets(const float* x32, int64_t ld, const double* mean,
                                  const int32_t* slot_tgt, int64_t slots, int T, float* Y,
                                  int64_t ldy, cudaStream_t st);

@@ -27,6 +27,8 @@
 
 #include <cuda_fp16.h>
 
+#include <algorithm>
+
 namespace cmb {
 
 namespace {
@@ -930,6 +932,51 @@ __global__ void __launch_bounds__(kFixWarps * 32) lookup_fixup_kernel(LookupArgs
   }
 }
 
+// ---------------------------------------------------------------- materialised predictions
+// lookup_batch(want_predictions=True) of the cross map (prediction.py:145-153,
+// ccm.py:148-149) for a caller-given set of (library, target) pairs, from the
+// SAME tables and centred targets the rho lookup used (so the predictions are
+// the ones behind rho).  One warp per pair, lanes over embedded points:
+// p_t = sum_q w_q y[row_q] in fp32 (explicit last weight 1 - sum of the others
+// for k <= 3 records, as in rot_library_group), plus the target's mean back.
+// pred[pair][t] for t < n_E, NaN after.
+__global__ void predict_pairs_kernel(LookupArgs a, const int4* __restrict__ pairs, int64_t npairs, int64_t c0,
+                                     const double* __restrict__ shift, float* __restrict__ pred, int64_t ldp) {
+  const int lane = lane_id();
+  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t q = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32; q < npairs; q += nw) {
+    const int4 pr = pairs[q];  // (library index in the library list, target slot, E, output row)
+    const int E = pr.z, K = E + 1;
+    const int n = a.T - (E - 1) * a.tau;
+    const int R = rec_bytes(K), RO = rec_row_off(K);
+    const uint8_t* rec0 = a.tab[E] + (size_t)(pr.x - c0) * rec_lib_stride(K, n);
+    const float* __restrict__ ycol = a.Y + pr.y;
+    const double mu = shift[pr.y];
+    float* out = pred + (size_t)pr.w * ldp;
+    for (int t = lane; t < a.T; t += 32) {
+      if (t >= n) {
+        out[t] = __int_as_float(0x7fc00000);
+        continue;
+      }
+      const uint8_t* rp = rec0 + (size_t)t * R;
+      const float* w = reinterpret_cast<const float*>(rp);
+      const uint16_t* rw = reinterpret_cast<const uint16_t*>(rp + RO);
+      float ws = 0.f, p = 0.f;
+      for (int kk = 0; kk < K; ++kk) {
+        float wk;
+        if (rec_implicit(K) && kk == K - 1) {
+          wk = __fsub_rn(1.f, ws);
+        } else {
+          wk = __ldg(w + kk);
+          ws = __fadd_rn(ws, wk);
+        }
+        p = __fmaf_rn(wk, __ldg(ycol + (size_t)__ldg(rw + kk) * a.ldy), p);
+      }
+      out[t] = (float)((double)p + mu);
+    }
+  }
+}
+
 // fp16-target variant (opt-in, CMB_LOOKUP_FP16=1): the resident block holds 64
 // targets as fp16 scaled to [-1, 1] -- the same 128 bytes per sample row -- and
 // lane l owns targets 2l and 2l + 1, so every shared-memory wavefront (gathers,
@@ -1208,6 +1255,15 @@ cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   count_launch();
   kern<<<grid, kLookupWarps * 32, smem, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_predict_pairs(const LookupArgs& a, const int4* pairs, int64_t npairs, int64_t c0,
+                                 const double* shift, float* pred, int64_t ldp, cudaStream_t st) {
+  if (npairs == 0) return cudaSuccess;
+  count_launch();
+  const int64_t blocks = std::min<int64_t>((npairs + 7) / 8, 148 * 16);
+  predict_pairs_kernel<<<(unsigned)blocks, 256, 0, st>>>(a, pairs, npairs, c0, shift, pred, ldp);
   return cudaGetLastError();
 }
 

@@ -62,7 +62,7 @@ __global__ void demote_kernel(const double* __restrict__ x, int64_t N, int64_t T
 // subtraction), the perturbation M the kNN certification bounds.  Distances
 // are translation invariant; the exact fp64 paths use the uncentred x64.
 __global__ void demote_center_kernel(const double* __restrict__ x, int64_t T, float* __restrict__ y,
-                                     float* __restrict__ err) {
+                                     float* __restrict__ err, double* __restrict__ mu_out) {
   const int64_t s = blockIdx.x;
   __shared__ double wsum[32];
   __shared__ float wm[32];
@@ -76,6 +76,7 @@ __global__ void demote_center_kernel(const double* __restrict__ x, int64_t T, fl
     double tot = 0.0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) tot += wsum[q];
     s_mean = tot / (double)T;
+    if (mu_out) mu_out[s] = s_mean;
   }
   __syncthreads();
   const double mu = s_mean;
@@ -428,10 +429,26 @@ cudaError_t launch_demote(const double* x64, int64_t N, int64_t T, float* x32, f
 }
 
 cudaError_t launch_demote_center(const double* x64, int64_t N, int64_t T, float* x32, float* err_m,
-                                 cudaStream_t st) {
+                                 double* mu, cudaStream_t st) {
   if (N == 0) return cudaSuccess;
   count_launch();
-  demote_center_kernel<<<(unsigned)N, 256, 0, st>>>(x64, T, x32, err_m);
+  demote_center_kernel<<<(unsigned)N, 256, 0, st>>>(x64, T, x32, err_m, mu);
+  return cudaGetLastError();
+}
+
+__global__ void slot_shift_kernel(const double* __restrict__ mean, const double* __restrict__ mu,
+                                  const int32_t* __restrict__ slot_tgt, int64_t slots, double* __restrict__ shift) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= slots) return;
+  const int t = slot_tgt[s];
+  shift[s] = t < 0 ? 0.0 : (double)(float)mean[t] + (mu ? mu[t] : 0.0);
+}
+
+cudaError_t launch_slot_shift(const double* mean, const double* mu, const int32_t* slot_tgt, int64_t slots,
+                              double* shift, cudaStream_t st) {
+  if (slots == 0) return cudaSuccess;
+  count_launch();
+  slot_shift_kernel<<<(unsigned)((slots + 255) / 256), 256, 0, st>>>(mean, mu, slot_tgt, slots, shift);
   return cudaGetLastError();
 }
 

@@ -141,6 +141,28 @@ def xmap(values, e_star, tau: int = 1, layout: int = LAYOUT_LIB_MAJOR, dtype=np.
 NATIVE_T_MAX = 65535  # 16-bit neighbour rows in the cross-map table records (csrc/cmb_common.cuh)
 
 
+def xmap_predictions(values, e_star, pairs, tau: int = 1) -> tuple[np.ndarray, np.ndarray]:
+    """The cross map plus materialised predictions of the (library, target)
+    ``pairs`` (lookup_batch(want_predictions=True), prediction.py:145-153) from
+    the same device tables and targets as rho (cmb_xmap_predict).  Returns
+    (rho[lib, tgt] float32, pred float32 [len(pairs), T]; row p holds target
+    pairs[p][1]'s prediction at its n_E embedded points, NaN after them and for
+    pairs with an undefined series)."""
+    X = np.asarray(values, dtype=np.float64)
+    T, N = X.shape
+    est = np.array([0 if (e is None or int(e) <= 0) else int(e) for e in e_star], dtype=np.int32)
+    if est.size != N:
+        raise ParameterError(f"{est.size} dimensions for {N} series")
+    pl = np.ascontiguousarray([p[0] for p in pairs], dtype=np.int32)
+    pt = np.ascontiguousarray([p[1] for p in pairs], dtype=np.int32)
+    Xs = np.ascontiguousarray(X.T)
+    rho = np.empty((N, N), dtype=np.float32)
+    pred = np.empty((max(pl.size, 1), T), dtype=np.float32)
+    nat.call("cmb_xmap_predict", nat.device(), nat.ptr(Xs), N, T, nat.ptr(est), tau, nat.ptr(pl), nat.ptr(pt),
+             pl.size, nat.ptr(rho), LAYOUT_LIB_MAJOR, nat.ptr(pred), None)
+    return rho, pred[: pl.size]
+
+
 def _xmap_with_wide(Xs: np.ndarray, est: np.ndarray, wide: np.ndarray, tau: int, layout: int, dtype,
                     stats: dict | None) -> np.ndarray:
     """xmap when some targets are outside the fused kernels' formats.  The fused
@@ -210,19 +232,36 @@ def ccm_pairwise(data: Dataset, cfg: CcmConfig | None = None, workers: int | Non
             groups.setdefault(s, []).append(i)
     stats.distinct_e = len(groups)
     info: dict = {}
-    rho = xmap(X.T, [s or 0 for s in stars], cfg.tau, layout=LAYOUT_TGT_MAJOR, stats=info)
+    est = [s or 0 for s in stars]
+    predictions = None
+    native = max(est) <= NATIVE_E_MAX and data.length <= NATIVE_T_MAX
+    if cfg.emit_predictions and native:
+        # every defined (library, target) pair, in the reference's order
+        # (ccm.py:131-149: library, then E group, then target)
+        order = [(lib, t) for lib in range(n) if stars[lib] is not None
+                 for e in sorted(groups) for t in groups[e]]
+        t0 = time.perf_counter()
+        rho32, pred = xmap_predictions(X.T, est, order, cfg.tau)
+        rho = rho32.astype(np.float64)
+        info["seconds_lookup"] = time.perf_counter() - t0
+        predictions = {}
+        for p, (lib, t) in enumerate(order):
+            ne = data.length - (stars[t] - 1) * cfg.tau
+            predictions[(lib, t)] = pred[p, :ne].astype(np.float64)
+    else:
+        rho = xmap(X.T, est, cfg.tau, layout=LAYOUT_TGT_MAJOR, stats=info)
+        if cfg.emit_predictions:  # formats past the fused kernels: the device composition per (library, E)
+            predictions = {}
+            for lib in range(n):
+                if stars[lib] is None:
+                    continue
+                for e in sorted(groups):
+                    table = build_knn_table(data[lib], EmbeddingSpec(e, cfg.tau, e_max=cfg.e_max))
+                    outs = lookup_batch(table, [data[t] for t in groups[e]], want_predictions=True)
+                    for t, o in zip(groups[e], outs):
+                        if o.predicted is not None:
+                            predictions[(lib, t)] = o.predicted
     stats.seconds_table_build = info.get("seconds_table_build", 0.0)
     stats.seconds_lookup = info.get("seconds_lookup", 0.0)
     stats.tables_built = sum(1 for s in stars if s is not None) * len(groups)
-    predictions = None
-    if cfg.emit_predictions:
-        predictions = {}
-        for lib in range(n):
-            if stars[lib] is None:
-                continue
-            for e in sorted(groups):
-                table = build_knn_table(data[lib], EmbeddingSpec(e, cfg.tau, e_max=cfg.e_max))
-                outs = lookup_batch(table, [data[t] for t in groups[e]], want_predictions=True)
-                for t, o in zip(groups[e], outs):
-                    predictions[(lib, t)] = o.predicted
     return SkillMatrix(data.names, rho, stats=stats, predictions=predictions)
