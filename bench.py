@@ -139,22 +139,34 @@ def lookup_alg_bytes(estar: np.ndarray, n_libs: int, T: int, tau: int = 1) -> fl
     return tot
 
 
+def rec_bytes(k: int) -> int:
+    """Table record size (csrc/cmb_common.cuh rec_bytes)."""
+    if k <= 3:
+        return (4 * (k - 1) + 2 * k + 7) & ~7
+    b = 4 * ((k + 3) & ~3) + 2 * ((k + 7) & ~7)
+    return b if (b >> 4) & 1 else b + 16
+
+
 def lookup_alg_wavefronts(estar: np.ndarray, n_libs: int, T: int, tau: int = 1) -> float:
-    """Shared-memory wavefronts the lookup issues per step on this rank (the
-    binding resource, K3): per embedded point of a (library, 32-target
-    block) pair k gathers + the record's 8-byte broadcast loads (ceil(k/2) weight +
-    ceil(k/4) row loads; one load in all for k = 2) + the observed-value load,
-    shared by the two libraries a warp runs in lockstep (1/2 per pair).  The
-    one-library form matched ncu l1tex__data_pipe_lsu_wavefronts_mem_shared
-    within 2% (profiles/r01_lookup_ncu_summary.txt)."""
+    """Shared-memory wavefronts the rotated lookup issues per step on this rank
+    (K3): per embedded point and 32 (point, target) pairs, k gathers
+    (one conflict-free wavefront each), the observed value (shared by the two
+    libraries of a lockstep pair for k <= 12, else one), and the per-lane record
+    loads -- each lane loads its point's record once per 8 targets (k <= 12: 16
+    targets for the two-target path k = 9..12), i.e. R/32 (R/64) wavefronts."""
     tot = 0.0
     for E in np.unique(estar[estar > 0]):
         NE = int(np.sum(estar == E))
         nE = T - (int(E) - 1) * tau
         k = int(E) + 1
-        # record broadcasts: k <= 3 stores k - 1 weights (cmb_common.cuh rec_*)
-        rec = 1 if k == 2 else ((k - 1 if k == 3 else k) + 1) // 2 + (k + 3) // 4
-        tot += n_libs * ((NE + 31) // 32) * nE * (k + rec + 0.5)
+        R = rec_bytes(k)
+        if k <= 8:
+            per = k + 0.5 + R / 32
+        elif k <= 12:
+            per = k + 1.0 + R / 64
+        else:
+            per = k + 1.0 + R / 32
+        tot += n_libs * ((NE + 31) // 32) * nE * per
     return tot
 
 
@@ -595,7 +607,8 @@ def run_ours(args):
             "parity": parity, "estar_equals_fixture": estar_check,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "lookup_xmap_kernel", "peak_kind": peak_kind,
+                         "kernel": "lookup_xmap_kernel (rotated-lane path) + lookup_fixup_kernel",
+                         "peak_kind": peak_kind,
                          "alg_bytes_per_step": alg, "lookup_ms_per_step": t_look * 1e3},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": diag["kernel_launches"], "fp16_lookup_mode": fp16,
             "clocks": clk.summary(),
@@ -603,8 +616,9 @@ def run_ours(args):
                 "bound": "shared-memory wavefronts (the lookup's binding resource)",
                 "achieved": wf / t_look / 1e9, "unit": "G wavefronts/s",
                 "peak": n_sms * sm_clock_ghz(clk), "frac": wf / t_look / 1e9 / (n_sms * sm_clock_ghz(clk)),
-                "wavefronts_per_step": wf, "model": "1 wavefront/clk/SM; k gathers + record broadcasts + 1/2 "
-                                                    "observed load (shared by a library pair) per point and 32 pairs"},
+                "wavefronts_per_step": wf, "model": "1 wavefront/clk/SM; per point and 32 pairs: k gathers + the "
+                                                    "observed value (1/2 when two libraries share it) + per-lane "
+                                                    "record loads R/32 (R/64 for k = 9..12)"},
             "extra": {"edim_seconds": t_edim, "edim_series_per_s": N / t_edim,
                       "tables_ms_per_step": t_tables_step * 1e3, "lookup_ms_per_step": t_lookup_step * 1e3,
                       "exact_fallback_rows": diag["exact_fallback_rows"], "rows_checked": diag["rows_checked"]},
