@@ -575,6 +575,21 @@ def run_ours(args):
                "ms_per_step": el * 1e3}
         del host, Xe, xp
 
+    # ---- the drop-in Python API at the same size: P.xmap on the host (time,
+    #      series) float32 array, target-major float32 result in pageable numpy
+    #      memory (what a reference user switching to this package calls);
+    #      wall time of one call, reported beside e2e (which is the raw C ABI)
+    api = None
+    if not args.no_e2e and world == 1 and not native and os.environ.get("CMB_BENCH_API", "1") == "1":
+        XT = np.ascontiguousarray(X_host.T)
+        t0 = time.perf_counter()
+        r_api = P.xmap(XT, estar, 1, layout=P.LAYOUT_TGT_MAJOR, dtype=np.float32)
+        el = time.perf_counter() - t0
+        api = {"call": "paper_2105_12301_b200.xmap(values[T][N] float32, e_star, layout=LAYOUT_TGT_MAJOR, "
+                       "dtype=float32)", "seconds": el, "pairs_per_s": pairs / el,
+               "note": "one call, pageable numpy output (pinned bounce slabs inside libcmb200)"}
+        del r_api, XT
+
     # ---- CPU baseline (the stock reference path on the host cores) on whole
     #      library rows, which double as the parity check of this run's rho
     cpu = parity = None
@@ -610,7 +625,8 @@ def run_ours(args):
                          "kernel": "lookup_xmap_kernel (rotated-lane path) + lookup_fixup_kernel",
                          "peak_kind": peak_kind,
                          "alg_bytes_per_step": alg, "lookup_ms_per_step": t_look * 1e3},
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": diag["kernel_launches"], "fp16_lookup_mode": fp16,
+            "cpu_baseline": cpu, "e2e": e2e, "api_xmap": api, "gpu_launches": diag["kernel_launches"],
+            "fp16_lookup_mode": fp16,
             "clocks": clk.summary(),
             "roofline_smem": {
                 "bound": "shared-memory wavefronts (the lookup's binding resource)",

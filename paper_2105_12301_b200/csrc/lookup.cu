@@ -1116,7 +1116,12 @@ constexpr int kPairMaxK = 31;  // library pairs for every k (A/B: k <= 8 5.83 s,
 constexpr int kPairMaxKL2 = 1;
 constexpr int kQuadMaxK = 4;  // four libraries in lockstep for k <= 4
 constexpr int kRotPairMaxK = 8;  // rotated path: two libraries in lockstep (packed FFMA2) for k <= 8
-constexpr int kRot2MinK = 9;     // two-target rotated path (rot2_library_pairs) for 9 <= k <= 24
+// two-target rotated path (rot2_library_pairs) for 4 <= k <= 24 (where the stage
+// slots hold 8 records of two libraries: k <= 12 at T = 1,450); A/B at full
+// size on one box (lookup seconds): rot2 from k = 9 4.764, from k = 4 4.719;
+// library pairs up to k = 12 instead of rot2 4.969; OR-formed gather addresses
+// (LOP3 instead of IMAD) 4.851
+constexpr int kRot2MinK = 4;
 constexpr int kRot2MaxK = 24;
 
 // Rotated-lane lookup of one warp's libraries [lib0, lib0 + nl); returns the

@@ -24,9 +24,21 @@ t = P.build_knn_table(X[3], P.EmbeddingSpec(5, 1))        # RAW tile kernel
 t2 = P.build_knn_table(X[3], P.EmbeddingSpec(3, 2))       # RAW v4 (tau = 2)
 cv = P.ccm_sweep(X[:5].T, e[:5], [20, 80], samples=3)     # convergence tables + lookup
 cv2 = P.ccm_sweep(X[:3].T, e[:3], [30], samples=2, tau=2) # generic restricted tables
+# round 2 paths: rotated lookup with every (library, block) queued for the fp64
+# fixup, float64 inputs with an offset (cmb_xmap64), predictions from the xmap
+# tables (cmb_xmap_predict), the NCCL rank path with one rank (cmb_xmap_multi)
+os.environ["CMB_FIX_RATIO"] = "2"
+rfix = P.xmap(X.T, e, dtype=np.float32)
+os.environ.pop("CMB_FIX_RATIO")
+r64 = P.xmap((300.0 + 1e-3 * X).T, e)
+data = P.Dataset(tuple(P.TimeSeries(X[i], f"s{i}") for i in range(12)))
+mp = P.ccm_pairwise(data, P.CcmConfig(e_max=8, emit_predictions=True))
+from paper_2105_12301_b200.distributed import xmap_multi
+rm = xmap_multi(X.astype(np.float32), e, [0])
 with tempfile.TemporaryDirectory() as d:
     m = P.SkillMatrix([f"s{i}" for i in range(40)], np.nan_to_num(rho.astype(np.float64), nan=0.5))
     P.write_skill_matrix(m, Path(d) / "m.csv")           # GPU CSV formatter
     back = P.read_skill_matrix(Path(d) / "m.csv")
 print("ok", float(np.nanmean(rho)), float(np.nanmean(rho16)), float(np.nanmean(rl)), t.indices.shape,
-      t2.indices.shape, cv.shape, cv2.shape, back.rho.shape)
+      t2.indices.shape, cv.shape, cv2.shape, back.rho.shape, float(np.nanmax(np.abs(rfix - rho))),
+      float(np.nanmean(r64)), len(mp.predictions), float(np.nanmax(np.abs(rm - rho))))
