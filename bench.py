@@ -150,21 +150,19 @@ def rec_bytes(k: int) -> int:
 def lookup_alg_wavefronts(estar: np.ndarray, n_libs: int, T: int, tau: int = 1) -> float:
     """Shared-memory wavefronts the rotated lookup issues per step on this rank
     (K3): per embedded point and 32 (point, target) pairs, k gathers
-    (one conflict-free wavefront each), the observed value (shared by the two
-    libraries of a lockstep pair for k <= 3, else one), and the per-lane record
-    loads -- each lane loads its point's record once per 8 targets (16 targets
-    for the two-target path k = 4..12), i.e. R/32 (R/64) wavefronts."""
+    (one conflict-free wavefront each), the observed value (one per 32 pairs),
+    and the per-lane record loads -- each lane loads its point's record once
+    per 16 targets in the two-target path (k <= 24; once per 8 above), i.e.
+    R/64 (R/32) wavefronts."""
     tot = 0.0
     for E in np.unique(estar[estar > 0]):
         NE = int(np.sum(estar == E))
         nE = T - (int(E) - 1) * tau
         k = int(E) + 1
         R = rec_bytes(k)
-        if k <= 3:
-            per = k + 0.5 + R / 32
-        elif k <= 12:
+        if k <= 24:  # two-target path (12- / 8-warp class kernels, lookup_class_warps)
             per = k + 1.0 + R / 64
-        else:
+        else:        # one library per warp, 16 warps
             per = k + 1.0 + R / 32
         tot += n_libs * ((NE + 31) // 32) * nE * per
     return tot
@@ -633,8 +631,7 @@ def run_ours(args):
                 "achieved": wf / t_look / 1e9, "unit": "G wavefronts/s",
                 "peak": n_sms * sm_clock_ghz(clk), "frac": wf / t_look / 1e9 / (n_sms * sm_clock_ghz(clk)),
                 "wavefronts_per_step": wf, "model": "1 wavefront/clk/SM; per point and 32 pairs: k gathers + the "
-                                                    "observed value (1/2 when two libraries share it) + per-lane "
-                                                    "record loads R/32 (R/64 for k = 4..12)"},
+                                                    "observed value + per-lane record loads R/64 (R/32 for k > 24)"},
             "extra": {"edim_seconds": t_edim, "edim_series_per_s": N / t_edim,
                       "tables_ms_per_step": t_tables_step * 1e3, "lookup_ms_per_step": t_lookup_step * 1e3,
                       "exact_fallback_rows": diag["exact_fallback_rows"], "rows_checked": diag["rows_checked"]},

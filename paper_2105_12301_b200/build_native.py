@@ -23,7 +23,7 @@ BUILD = PKG / "_build"
 LIB = PKG / "libcmb200.so"
 SOURCES = ["knn_sweep.cu", "knn_w_a.cu", "knn_w_b.cu", "knn_w_c.cu", "knn_w_d.cu", "knn_w_e.cu",
            "knn_t_a.cu", "knn_t_b.cu", "knn_t_c.cu", "knn_t_d.cu",
-           "lookup.cu", "utils.cu", "convergence.cu", "io.cu", "cmb_api.cu"]
+           "lookup.cu", "lookup_r16_4_12.cu", "lookup_r16_13_20.cu", "lookup_r16_21_31.cu", "lookup_nr.cu", "lookup_h16.cu", "lookup_w12.cu", "lookup_w8.cu", "utils.cu", "convergence.cu", "io.cu", "cmb_api.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]

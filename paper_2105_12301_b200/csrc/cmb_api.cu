@@ -439,6 +439,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
 
   const char* rot_env = getenv("CMB_LOOKUP_ROT");
   const char* fix_env = getenv("CMB_FIX_RATIO");
+  const char* split_env = getenv("CMB_LOOKUP_SPLIT");  // 0: every k in one 16-warp launch
   CMB_CUDA(ctx->buf[B_FIX].ensure(16 + sizeof(int2) * (size_t)kFixCap));
   int64_t fixups = 0;
   EventSet evs;
@@ -501,11 +502,61 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     la.fix_count = ctx->buf[B_FIX].as<int>();
     la.fix_cap = kFixCap;
     la.fix_ratio = fix_env ? atof(fix_env) : 0.0625;
-    CMB_CUDA(cudaMemsetAsync(la.counter, 0, sizeof(int), st));
+    la.warps = 0;
     CMB_CUDA(cudaMemsetAsync(la.fix_count, 0, sizeof(int), st));
     int dev_sms = 148;
     cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, ctx->dev);
-    CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(items, dev_sms), st));
+    // one launch per warp-count class (lookup_class_warps): the groups of a
+    // class, their own work items and stage size; a class whose two-target
+    // stage does not fit (long series) goes to the 16-warp launch
+    auto launch_all = [&](bool split) -> int {
+      // classes 0-3: 16-warp launches per k range (lookup_r16_range, one
+      // instantiation unit each); 4 / 5: the 12- / 8-warp two-target kernels
+      constexpr int NC = 6;
+      LookupArgs cls[NC];
+      const int cw[NC] = {kLookupWarps, kLookupWarps, kLookupWarps, kLookupWarps, 12, 8};
+      for (int c = 0; c < NC; ++c) {
+        cls[c] = la;
+        cls[c].ngroups = 0;
+        cls[c].warps = c < 4 ? 0 : cw[c];
+      }
+      int mrec[NC] = {0, 0, 0, 0, 0, 0};
+      const bool resident = stage != kNonResidentStage;
+      for (int g = 0; g < la.ngroups; ++g) {
+        const int k = la.g_E[g] + 1;
+        // the non-resident and 16-bit kernels cover every k in one launch
+        int c = (resident && !h16) ? lookup_r16_range(k) : 0;
+        if (split && resident && !h16 && la.rot == 2) {
+          const int w = lookup_class_warps(k);
+          const int cand = w == 12 ? 4 : (w == 8 ? 5 : -1);
+          if (cand > 0 && lookup_rot2_fits(lookup_stage_bytes((int)T, rec_bytes(k), w), k)) c = cand;
+        }
+        const int q = cls[c].ngroups++;
+        cls[c].g_E[q] = la.g_E[g];
+        cls[c].g_blk0[q] = la.g_blk0[g];
+        cls[c].g_nblk[q] = la.g_nblk[g];
+        mrec[c] = std::max(mrec[c], rec_bytes(k));
+      }
+      for (int c = 0; c < NC; ++c) {
+        LookupArgs& L = cls[c];
+        if (L.ngroups == 0) continue;
+        L.LS = 4 * cw[c];
+        L.n_lsub = (int)((nc + L.LS - 1) / L.LS);
+        int64_t it = 0;
+        for (int g = 0; g < L.ngroups; ++g) {
+          L.g_item0[g] = it;
+          it += (int64_t)L.n_lsub * L.g_nblk[g];
+        }
+        L.g_item0[L.ngroups] = it;
+        L.n_items = it;
+        L.stage_bytes = c < 4 ? stage : lookup_stage_bytes((int)T, mrec[c], cw[c]);
+        CMB_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(int), st));
+        CMB_CUDA(launch_lookup_xmap(L, (int)std::min<int64_t>(it, dev_sms), st));
+      }
+      return CMB_OK;
+    };
+    const bool split = !(split_env && split_env[0] == '0');
+    CMB_TRY(launch_all(split));
     if (la.rot) CMB_CUDA(launch_lookup_fixup(la, st));
     if (!pairs.empty()) {
       const auto lo_it = std::lower_bound(pairs.begin(), pairs.end(), (int)c0,
@@ -531,8 +582,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
         // more ill-conditioned pairs than the queue holds (a pathological chunk):
         // redo the chunk with the shifted-moment lookup, which needs no fixups
         la.rot = 0;
-        CMB_CUDA(cudaMemsetAsync(la.counter, 0, sizeof(int), st));
-        CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(items, dev_sms), st));
+        CMB_TRY(launch_all(false));
         CMB_CUDA(cudaEventRecord(ev[2], st));
         CMB_CUDA(cudaEventSynchronize(ev[2]));
       }

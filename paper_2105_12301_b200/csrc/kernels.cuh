@@ -79,6 +79,7 @@ struct LookupArgs {
   // ill-conditioned in the unshifted fp32 sums is queued here as (library in
   // chunk, first slot of the block) and recomputed in fp64 by lookup_fixup_kernel
   int rot;
+  int warps;                 // CTA warps of this launch (0 = kLookupWarps; 12 / 8: rot2 class kernels)
   double fix_ratio;          // queue when m2p <= fix_ratio * sum p^2
   int2* fix;
   int* fix_count;
@@ -88,8 +89,33 @@ struct LookupArgs {
 constexpr int kLookupWarps = 16;
 // stage size that selects the non-resident (targets in L2) lookup variant
 constexpr int kNonResidentStage = 4096 + 16;
-int lookup_stage_bytes(int T, int max_rec_bytes);
+int lookup_stage_bytes(int T, int max_rec_bytes, int warps = kLookupWarps);
+// two-target rotated path feasible for k at this stage size
+bool lookup_rot2_fits(int stage_bytes, int k);
+// k <= 3 through the 12-warp two-target path too (else the 16-warp library pairs)
+constexpr bool kSmallKRot2 = true;
+// CTA warps per neighbour-count class of the resident fp32 lookup.  Fewer warps
+// leave larger stage slots, so the two-target path (8 records of two libraries
+// per slot) fits for larger k, and more registers per thread.  A/B at full
+// size on one box (lookup seconds): every k in one 16-warp kernel 4.705, every
+// k with 12 warps 4.543, with 8 4.462; classes 16 (k <= 3) / 12 (4..16) / 8
+// (17..24) 4.126; k <= 3 also with 12 warps (two-target path) 3.974.
+constexpr int lookup_class_warps(int k) {
+  return k <= 3 ? (kSmallKRot2 ? 12 : 16) : (k <= 16 ? 12 : (k <= 24 ? 8 : 16));
+}
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st);
+// per-instantiation launchers (lookup*.cu; smem = dynamic shared bytes)
+cudaError_t launch_lookup_resident16(const LookupArgs& a, int grid, int smem, cudaStream_t st);
+// k ranges of the 16-warp resident kernel's instantiation units
+constexpr int lookup_r16_range(int k) { return k <= 3 ? 0 : (k <= 12 ? 1 : (k <= 20 ? 2 : 3)); }
+cudaError_t launch_lookup_r16_2_3(const LookupArgs& a, int grid, int smem, cudaStream_t st);
+cudaError_t launch_lookup_r16_4_12(const LookupArgs& a, int grid, int smem, cudaStream_t st);
+cudaError_t launch_lookup_r16_13_20(const LookupArgs& a, int grid, int smem, cudaStream_t st);
+cudaError_t launch_lookup_r16_21_31(const LookupArgs& a, int grid, int smem, cudaStream_t st);
+cudaError_t launch_lookup_nonresident(const LookupArgs& a, int grid, int smem, cudaStream_t st);
+cudaError_t launch_lookup_h16(const LookupArgs& a, int grid, int smem, cudaStream_t st);
+cudaError_t launch_lookup_w12(const LookupArgs& a, int grid, int smem, cudaStream_t st);
+cudaError_t launch_lookup_w8(const LookupArgs& a, int grid, int smem, cudaStream_t st);
 // predictions of (library, target) pairs from the chunk's tables: pairs[q] =
 // (library list index, target slot, E, output row), libraries [c0, c0 + nlib);
 // pred[row][t] = sum w y (centred fp32 targets) + shift[slot]

@@ -125,6 +125,7 @@ def test_bench_roofline_models():
     # E=1: N_E=2, n_E=10, k=2; E=2: N_E=1, n_E=9, k=3  (B_pair = 4 n + 8 n k / N_E + 4)
     want = libs * (2 * (4 * 10 + 4) + 8 * 10 * 2) + libs * (1 * (4 * 9 + 4) + 8 * 9 * 3)
     assert bench.lookup_alg_bytes(estar, libs, T) == want
-    # one 32-target block per E group; per point k gathers + record loads + the observed
-    # load shared by a library pair (k=2: 1 record load; k=3: 1 weight + 1 row load)
-    assert bench.lookup_alg_wavefronts(estar, libs, T) == libs * (10 * (2 + 1 + 0.5) + 9 * (3 + 2 + 0.5))
+    # one 32-target block per E group; per point and 32 pairs k gathers + the observed
+    # value + R/64 record loads (two-target path: k=2 records 8 B, k=3 16 B)
+    assert bench.lookup_alg_wavefronts(estar, libs, T) == libs * (10 * (2 + 1 + 8 / 64) + 9 * (3 + 1 + 16 / 64))
+    assert bench.rec_bytes(2) == 8 and bench.rec_bytes(4) == 48 and bench.rec_bytes(21) == 144
