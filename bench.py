@@ -317,8 +317,18 @@ def run_reference(args):
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": stock.workers, "kind": stock.kind,
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "step_definition": "one whole library row (all targets) per step; value = pairs/s of those rows"}
+            "step_definition": "one whole library row (all targets) per step; value = pairs/s of those rows",
+            "libcmb200_mapped": _libcmb_mapped()}
     print(json.dumps(line), flush=True)
+
+
+def _libcmb_mapped() -> bool:
+    """Whether this process mapped the repo's libcmb200.so (the reference arm must not)."""
+    try:
+        with open("/proc/self/maps") as fh:
+            return any("libcmb200" in ln for ln in fh)
+    except OSError:
+        return False
 
 
 def workload_config(args, valid, estar):
