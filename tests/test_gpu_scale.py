@@ -124,3 +124,19 @@ def test_native_nccl_rank_path_single_rank():
     assert np.array_equal(rho.cpu().numpy(), ref, equal_nan=True)
     nat.call("cmb_nccl_destroy", 0)
     assert np.array_equal(xmap_multi(X, est, [0]), ref, equal_nan=True)
+
+
+@pytest.mark.parametrize("T,Es", [(1450, (1, 3, 10, 17, 24)), (1640, (1, 5, 14, 20)), (400, (2, 25, 28))])
+def test_lookup_warp_classes_and_fallbacks(T, Es):
+    """The lookup's launch classes (12-warp k <= 16, 8-warp k 17..24 on the
+    two-target path) and their fallbacks -- 16-warp k-range kernels when a
+    class's stage does not fit near the resident-length limit (T = 1,640) and
+    for k > 24 -- against the oracle on whole library rows."""
+    N = 70
+    X = P.mixed_dataset(N, T, seed=77, dtype=np.float32).astype(np.float64)
+    est = np.array([Es[i % len(Es)] for i in range(N)], dtype=np.int32)
+    rho = P.xmap(X.T, est)
+    libs = [3, 41]
+    ref = O.xmap_rows(list(X), est.tolist(), libs, 1, workers=WORKERS)
+    worst = _check_rows(rho[libs], ref)
+    assert worst <= RHO_TOL, worst
