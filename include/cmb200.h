@@ -217,13 +217,15 @@ int cmb_csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, i
  * per record -> out[row][ncols].  mode 1 (read_skill_matrix): a label cell then
  * ncols cells, "NA" = NaN; labels of rows < cap_rows go to labels/label_spans,
  * later rows are only counted.  *nrows = records read.  Cells with non-ASCII
- * bytes are left NaN and listed as (row, col) in defer[] (*ndefer): the caller
- * converts them with float() (which accepts Unicode digits).  On a non-zero
+ * bytes are left NaN and listed as (row, col, offset, length) in defer[]
+ * (*ndefer), their unquoted text in defer_text: the caller converts them with
+ * float() (which accepts Unicode digits).  On a non-zero
  * status err = {status, record (0 = first after the header), column, cells of
  * the record, length of the cell text copied to err_text}.                  */
 int cmb_csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out, int64_t cap_rows,
                  int64_t* nrows, char* labels, int64_t labels_cap, int64_t* label_spans, int64_t* defer,
-                 int64_t defer_cap, int64_t* ndefer, char* err_text, int64_t err_cap, int64_t* err);
+                 int64_t defer_cap, char* defer_text, int64_t defer_text_cap, int64_t* ndefer, char* err_text,
+                 int64_t err_cap, int64_t* err);
 
 #ifdef __cplusplus
 }

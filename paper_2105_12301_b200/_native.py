@@ -58,8 +58,8 @@ _SIGNATURES = {
     "cmb_format_skill_csv": ([C.c_int, _P, C.c_int, C.c_int, _i64, _i64, _i64, _i64, _P, _P, _P, _i64,
                               _P], C.c_int),
     "cmb_csv_header": ([_P, _i64, _P, _i64, _P, _i64, _P, _P], C.c_int),
-    "cmb_csv_body": ([_P, _i64, C.c_int, _i64, _P, _i64, _P, _P, _i64, _P, _P, _i64, _P, _P, _i64, _P],
-                     C.c_int),
+    "cmb_csv_body": ([_P, _i64, C.c_int, _i64, _P, _i64, _P, _P, _i64, _P, _P, _i64, _P, _i64, _P, _P, _i64,
+                      _P], C.c_int),
 }
 
 EXPORTS = tuple(_SIGNATURES)

@@ -1502,12 +1502,13 @@ int cmb_csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, i
 
 int cmb_csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out, int64_t cap_rows,
                  int64_t* nrows, char* labels, int64_t labels_cap, int64_t* label_spans, int64_t* defer,
-                 int64_t defer_cap, int64_t* ndefer, char* err_text, int64_t err_cap, int64_t* err) {
+                 int64_t defer_cap, char* defer_text, int64_t defer_text_cap, int64_t* ndefer, char* err_text,
+                 int64_t err_cap, int64_t* err) {
   if (!buf || len < 0 || (mode != 0 && mode != 1) || ncols < (mode == 1 ? 1 : 0) || !out || !nrows || !ndefer || !err ||
       (mode == 1 && (!labels || !label_spans)))
     return CSV_CAPACITY;
   return csv_body(buf, len, mode, ncols, out, cap_rows, nrows, labels, labels_cap, label_spans, defer, defer_cap,
-                  ndefer, err_text, err_cap, err);
+                  defer_text, defer_text_cap, ndefer, err_text, err_cap, err);
 }
 
 }  // extern "C"

@@ -364,10 +364,11 @@ int csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, int64
 
 int csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out, int64_t cap_rows, int64_t* nrows,
              char* labels, int64_t labels_cap, int64_t* label_spans, int64_t* defer, int64_t defer_cap,
-             int64_t* ndefer, char* err_text, int64_t err_cap, int64_t* err) {
+             char* defer_text, int64_t defer_text_cap, int64_t* ndefer, char* err_text, int64_t err_cap,
+             int64_t* err) {
   CsvCursor cur(buf, len);
   const int64_t want = ncols + (mode == 1 ? 1 : 0);
-  int64_t row = 0, lab = 0, nd = 0;
+  int64_t row = 0, lab = 0, nd = 0, dtext = 0;
   auto fail = [&](int code, int64_t col, const char* t, int64_t tl, int64_t ncell) {
     err[0] = code;
     err[1] = row;
@@ -404,8 +405,13 @@ int csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out,
         // float() also takes Unicode digits and blanks: the caller converts
         if (nd >= defer_cap) return fail(CSV_CAPACITY, col, nullptr, 0, 0);
         if (row >= cap_rows) return fail(mode == 1 ? CSV_BAD_CELL : CSV_CAPACITY, col, f, fl, 0);
-        defer[2 * nd] = row;
-        defer[2 * nd + 1] = col;
+        if (dtext + fl > defer_text_cap) return fail(CSV_CAPACITY, col, nullptr, 0, 0);
+        memcpy(defer_text + dtext, f, (size_t)fl);
+        defer[4 * nd] = row;
+        defer[4 * nd + 1] = col;
+        defer[4 * nd + 2] = dtext;
+        defer[4 * nd + 3] = fl;
+        dtext += fl;
         ++nd;
         out[row * ncols + col] = __builtin_nan("");
         continue;

@@ -176,6 +176,7 @@ int csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, int64
                int64_t* ncells, int64_t* body_off);
 int csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out, int64_t cap_rows, int64_t* nrows,
              char* labels, int64_t labels_cap, int64_t* label_spans, int64_t* defer, int64_t defer_cap,
-             int64_t* ndefer, char* err_text, int64_t err_cap, int64_t* err);
+             char* defer_text, int64_t defer_text_cap, int64_t* ndefer, char* err_text, int64_t err_cap,
+             int64_t* err);
 
 }  // namespace cmb

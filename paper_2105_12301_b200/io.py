@@ -57,14 +57,24 @@ def _raw(path: Path) -> bytes:
 
 def _header(raw: bytes, path: Path) -> tuple[list[str], int]:
     """Unquoted cells of the first record and the offset of the second
-    (cmb_csv_header; the csv module's excel dialect)."""
-    buf = np.frombuffer(raw, dtype=np.uint8)
-    max_cells = int(np.count_nonzero(buf == 44)) + 1
-    text = np.empty(max(len(raw), 1), dtype=np.uint8)
-    spans = np.empty(2 * max_cells, dtype=np.int64)
-    ncells, body = np.zeros(1, np.int64), np.zeros(1, np.int64)
-    rc = nat.load().cmb_csv_header(nat.ptr(buf if buf.size else np.zeros(1, np.uint8)), len(raw), nat.ptr(text), text.size,
-                                   nat.ptr(spans), max_cells, nat.ptr(ncells), nat.ptr(body))
+    (cmb_csv_header; the csv module's excel dialect).  Buffers are sized from a
+    window that starts at the first line and doubles when the record (a quoted
+    field with line breaks) runs past it, never from the whole file."""
+    full = np.frombuffer(raw, dtype=np.uint8)
+    nl = raw.find(b"\n")
+    win = len(raw) if nl < 0 else nl + 1
+    while True:
+        view = full[:win] if win < full.size else full
+        max_cells = int(np.count_nonzero(view == 44)) + 1
+        text = np.empty(max(view.size, 1), dtype=np.uint8)
+        spans = np.empty(2 * max_cells, dtype=np.int64)
+        ncells, body = np.zeros(1, np.int64), np.zeros(1, np.int64)
+        rc = nat.load().cmb_csv_header(nat.ptr(full if full.size else np.zeros(1, np.uint8)), len(raw),
+                                       nat.ptr(text), text.size, nat.ptr(spans), max_cells, nat.ptr(ncells),
+                                       nat.ptr(body))
+        if rc != 7 or win >= full.size:  # 7 = CMB_CSV_CAPACITY: widen the window
+            break
+        win = min(full.size, 2 * win)
     if rc == _CSV_EMPTY:
         raise CsvFormatError(f"{path}: empty file")
     _raise_field_limit(rc)
@@ -86,45 +96,41 @@ class _Body:
     the cells left for Python's float() (non-ASCII), and the first error."""
 
     def __init__(self, raw: bytes, off: int, mode: int, ncols: int, cap_rows: int | None):
-        buf = np.frombuffer(raw, dtype=np.uint8)[off:]
+        buf = np.ascontiguousarray(np.frombuffer(raw, dtype=np.uint8)[off:])
         records = int(np.count_nonzero(buf == 10) + np.count_nonzero(buf == 13)) + 1
         cap = records if cap_rows is None else cap_rows
         self.values = np.full((max(cap, 1), max(ncols, 1)), np.nan)
-        labels = np.empty(max(buf.size, 1), dtype=np.uint8)
-        lspans = np.zeros((max(cap, 1), 2), dtype=np.int64)
+        lspans = np.zeros((max(cap, 1) if mode == 1 else 1, 2), dtype=np.int64)
         ndef_cap = int(np.count_nonzero(buf >= 0x80)) + 1
-        defer = np.zeros((ndef_cap, 2), dtype=np.int64)
+        defer = np.zeros((ndef_cap, 4), dtype=np.int64)
         err = np.zeros(8, dtype=np.int64)
         err_text = np.empty(_FIELD_LIMIT + 1, dtype=np.uint8)
         nrows, ndef = np.zeros(1, np.int64), np.zeros(1, np.int64)
-        body = raw[off:]
-        bptr = nat.ptr(np.ascontiguousarray(buf)) if buf.size else nat.ptr(np.zeros(1, np.uint8))
-        self.rc = nat.load().cmb_csv_body(bptr, len(body), mode, ncols, nat.ptr(self.values), cap, nat.ptr(nrows),
-                                          nat.ptr(labels), labels.size, nat.ptr(lspans), nat.ptr(defer), ndef_cap,
-                                          nat.ptr(ndef), nat.ptr(err_text), err_text.size, nat.ptr(err))
+        bptr = nat.ptr(buf) if buf.size else nat.ptr(np.zeros(1, np.uint8))
+        # row labels (mode 1) and the text of non-ASCII cells: small buffers that
+        # grow (the pass is re-run) only if a file needs more
+        lab_cap = min(buf.size, 1 << 22) if mode == 1 else 1
+        txt_cap = min(buf.size, 1 << 20) if ndef_cap > 1 else 1
+        while True:
+            labels = np.empty(max(lab_cap, 1), dtype=np.uint8)
+            dtext = np.empty(max(txt_cap, 1), dtype=np.uint8)
+            self.rc = nat.load().cmb_csv_body(bptr, buf.size, mode, ncols, nat.ptr(self.values), cap,
+                                              nat.ptr(nrows), nat.ptr(labels), labels.size, nat.ptr(lspans),
+                                              nat.ptr(defer), ndef_cap, nat.ptr(dtext), dtext.size, nat.ptr(ndef),
+                                              nat.ptr(err_text), err_text.size, nat.ptr(err))
+            if self.rc != 7 or (lab_cap >= buf.size and txt_cap >= buf.size):  # 7: a buffer was too small
+                break
+            lab_cap = min(buf.size, 4 * lab_cap) if mode == 1 else 1
+            txt_cap = min(buf.size, 4 * txt_cap) if ndef_cap > 1 else 1
         _raise_field_limit(self.rc)
         self.nrows = int(nrows[0])
         self.err_row, self.err_col, self.err_cells = int(err[1]), int(err[2]), int(err[3])
         self.err_text = err_text[: int(err[4])].tobytes().decode("utf-8", errors="surrogateescape")
-        self.deferred = [(int(r), int(c)) for r, c in defer[: int(ndef[0])]]
-        if self.deferred:  # their text: re-read those records with the field spans of the same reader
-            self._deferred_text(body, mode)
-        lb = labels.tobytes()
+        dt = dtext.tobytes() if int(ndef[0]) else b""
+        self.deferred = [(int(r), int(c)) for r, c, _, _ in defer[: int(ndef[0])]]
+        self.deferred_text = [dt[o:o + n].decode("utf-8") for _, _, o, n in defer[: int(ndef[0])]]
+        lb = labels.tobytes() if mode == 1 else b""
         self.labels = [lb[a:a + b].decode("utf-8") for a, b in lspans[: min(self.nrows, cap)]] if mode == 1 else []
-
-    def _deferred_text(self, body: bytes, mode: int) -> None:
-        """Cell text of the deferred cells: a second pass of the header reader
-        over each record (the same tokenizer), record by record."""
-        want = {r for r, _ in self.deferred}
-        texts, pos, rec = {}, 0, 0
-        while rec <= max(want) and pos < len(body):
-            cells, nxt = _header(body[pos:], Path("<record>"))
-            if rec in want:
-                texts[rec] = cells
-            pos += nxt
-            rec += 1
-        shift = 1 if mode == 1 else 0
-        self.deferred_text = [texts[r][c + shift] for r, c in self.deferred]
 
 
 def load_csv(path) -> Dataset:
@@ -143,7 +149,7 @@ def load_csv(path) -> Dataset:
     if dup:
         raise CsvFormatError(f"{path}: duplicate column names: {dup}")
     b = _Body(raw, off, 0, len(names), None)
-    for (r, c), text in zip(b.deferred, getattr(b, "deferred_text", [])):
+    for (r, c), text in zip(b.deferred, b.deferred_text):
         where = f"{path}: row {r + 2}, column {names[c]!r}"
         try:
             v = float(text)
@@ -239,7 +245,7 @@ def read_skill_matrix(path) -> SkillMatrix:
         raise CsvFormatError(f"{path}: no target columns in header")
     n = len(names)
     b = _Body(raw, off, 1, n, n)
-    for (r, c), text in zip(b.deferred, getattr(b, "deferred_text", [])):
+    for (r, c), text in zip(b.deferred, b.deferred_text):
         try:
             v = float(text)
         except ValueError:
