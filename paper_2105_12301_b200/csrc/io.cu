@@ -218,63 +218,75 @@ constexpr int64_t kFieldLimit = 131072;  // csv.field_size_limit() default
 struct CsvCursor {
   const char* b;
   int64_t n, pos = 0;
-  std::string field;                      // unquoted text of the current field
-  std::vector<std::pair<int64_t, int64_t>> spans;  // fields of the record in `text`
+  // fields of the current record: unquoted ones point into the data (off into
+  // b), quoted ones into `text` (their unescaped copy)
+  struct Span {
+    int64_t off, len;
+    bool quoted;
+  };
+  std::vector<Span> spans;
   std::string text;
   bool oversize = false;
   CsvCursor(const char* buf, int64_t len) : b(buf), n(len) {}
+
+  const char* fptr(size_t c) const { return spans[c].quoted ? text.data() + spans[c].off : b + spans[c].off; }
+  int64_t flen(size_t c) const { return spans[c].len; }
 
   // next record into spans/text; false at the end of the data
   bool next() {
     spans.clear();
     text.clear();
     if (pos >= n) return false;
-    enum { START_FIELD, IN_FIELD, IN_QUOTED, QUOTE_IN_QUOTED } st = START_FIELD;
     // a line break at the start of a record: a record without cells
     if (b[pos] == '\n' || b[pos] == '\r') {
       pos += (b[pos] == '\r' && pos + 1 < n && b[pos + 1] == '\n') ? 2 : 1;
       return true;
     }
-    field.clear();
-    auto save = [&]() {
-      if ((int64_t)field.size() > kFieldLimit) oversize = true;
-      spans.push_back({(int64_t)text.size(), (int64_t)field.size()});
-      text += field;
-      field.clear();
-    };
-    while (pos < n) {
-      const char c = b[pos];
-      const bool eol = c == '\n' || c == '\r';
-      switch (st) {
-        case START_FIELD:
-          if (eol) { save(); goto record_end; }
-          if (c == '"') st = IN_QUOTED;
-          else if (c == ',') save();
-          else { field.push_back(c); st = IN_FIELD; }
-          break;
-        case IN_FIELD:
-          if (eol) { save(); goto record_end; }
-          if (c == ',') { save(); st = START_FIELD; }
-          else field.push_back(c);
-          break;
-        case IN_QUOTED:
-          if (c == '"') st = QUOTE_IN_QUOTED;
-          else field.push_back(c);
-          break;
-        case QUOTE_IN_QUOTED:
-          if (c == '"') { field.push_back('"'); st = IN_QUOTED; }
-          else if (c == ',') { save(); st = START_FIELD; }
-          else if (eol) { save(); goto record_end; }
-          else { field.push_back(c); st = IN_FIELD; }
-          break;
+    for (;;) {
+      // one field starting at pos
+      if (pos < n && b[pos] == '"') {
+        // quoted: '""' is one '"', line breaks kept, text after the closing
+        // quote appended up to the delimiter (non-strict)
+        const int64_t off = (int64_t)text.size();
+        ++pos;
+        bool in_quotes = true;
+        while (pos < n) {
+          const char c = b[pos];
+          if (in_quotes) {
+            if (c == '"') {
+              if (pos + 1 < n && b[pos + 1] == '"') { text.push_back('"'); pos += 2; continue; }
+              in_quotes = false;
+              ++pos;
+              continue;
+            }
+            text.push_back(c);
+            ++pos;
+          } else {
+            if (c == ',' || c == '\n' || c == '\r') break;
+            text.push_back(c);
+            ++pos;
+          }
+        }
+        spans.push_back({off, (int64_t)text.size() - off, true});
+      } else {
+        int64_t e = pos;
+        while (e < n && b[e] != ',' && b[e] != '\n' && b[e] != '\r') ++e;
+        spans.push_back({pos, e - pos, false});
+        pos = e;
       }
-      ++pos;
+      if (spans.back().len > kFieldLimit) oversize = true;
+      if (pos >= n) return true;  // end of data (an open quoted field ends here)
+      if (b[pos] == ',') {
+        ++pos;
+        if (pos >= n) {  // a trailing delimiter: one more, empty field
+          spans.push_back({pos, 0, false});
+          return true;
+        }
+        continue;
+      }
+      pos += (b[pos] == '\r' && pos + 1 < n && b[pos + 1] == '\n') ? 2 : 1;
+      return true;
     }
-    save();  // end of data (an open quoted field ends here, non-strict)
-    return true;
-  record_end:
-    pos += (b[pos] == '\r' && pos + 1 < n && b[pos + 1] == '\n') ? 2 : 1;
-    return true;
   }
 };
 
@@ -298,6 +310,25 @@ int py_float(const char* s, int64_t len, double* v) {
   };
   if (ieq("inf") || ieq("infinity")) { *v = neg ? -HUGE_VAL : HUGE_VAL; return 0; }
   if (ieq("nan")) { *v = neg ? -__builtin_nan("") : __builtin_nan(""); return 0; }
+  // common case: no '_' separator -- std::from_chars straight on the text
+  // (it takes exactly float()'s decimal forms once the sign is removed)
+  if ((s[a] >= '0' && s[a] <= '9') || s[a] == '.') {
+    bool under = false;
+    for (int64_t q = a; q < e && !under; ++q) under = s[q] == '_';
+    if (!under) {
+      double r = 0.0;
+      auto res = std::from_chars(s + a, s + e, r);
+      if (res.ptr != s + e) return 1;
+      if (res.ec == std::errc::result_out_of_range) {
+        std::string t(s + a, (size_t)(e - a));
+        r = strtod(t.c_str(), nullptr);
+      } else if (res.ec != std::errc()) {
+        return 1;
+      }
+      *v = neg ? -r : r;
+      return 0;
+    }
+  }
   // digits ('_' only between two digits), '.', exponent
   char tmp[512];
   std::string big;
@@ -351,11 +382,15 @@ int csv_header(const char* buf, int64_t len, char* text, int64_t text_cap, int64
   CsvCursor cur(buf, len);
   if (!cur.next()) return CSV_EMPTY;
   if (cur.oversize) return CSV_FIELD_LIMIT;
-  if ((int64_t)cur.spans.size() > max_cells || (int64_t)cur.text.size() > text_cap) return CSV_CAPACITY;
-  memcpy(text, cur.text.data(), cur.text.size());
+  int64_t tot = 0;
+  for (size_t q = 0; q < cur.spans.size(); ++q) tot += cur.flen(q);
+  if ((int64_t)cur.spans.size() > max_cells || tot > text_cap) return CSV_CAPACITY;
+  int64_t o = 0;
   for (size_t q = 0; q < cur.spans.size(); ++q) {
-    spans[2 * q] = cur.spans[q].first;
-    spans[2 * q + 1] = cur.spans[q].second;
+    memcpy(text + o, cur.fptr(q), (size_t)cur.flen(q));
+    spans[2 * q] = o;
+    spans[2 * q + 1] = cur.flen(q);
+    o += cur.flen(q);
   }
   *ncells = (int64_t)cur.spans.size();
   *body_off = cur.pos;
@@ -384,19 +419,18 @@ int csv_body(const char* buf, int64_t len, int mode, int64_t ncols, double* out,
     if (cur.oversize) return fail(CSV_FIELD_LIMIT, 0, nullptr, 0, 0);
     const int64_t nc = (int64_t)cur.spans.size();
     if (nc != want) return fail(CSV_WIDTH, 0, nullptr, 0, nc);
-    const char* t = cur.text.data();
     if (mode == 1 && row < cap_rows) {  // rows past the matrix only count (then a row-name mismatch)
-      const auto sp = cur.spans[0];
-      if (lab + sp.second > labels_cap) return fail(CSV_CAPACITY, 0, nullptr, 0, 0);
-      memcpy(labels + lab, t + sp.first, (size_t)sp.second);
+      const int64_t ll = cur.flen(0);
+      if (lab + ll > labels_cap) return fail(CSV_CAPACITY, 0, nullptr, 0, 0);
+      memcpy(labels + lab, cur.fptr(0), (size_t)ll);
       label_spans[2 * row] = lab;
-      label_spans[2 * row + 1] = sp.second;
-      lab += sp.second;
+      label_spans[2 * row + 1] = ll;
+      lab += ll;
     }
     for (int64_t c = (mode == 1 ? 1 : 0); c < nc; ++c) {
       const int64_t col = mode == 1 ? c - 1 : c;
-      const char* f = t + cur.spans[c].first;
-      const int64_t fl = cur.spans[c].second;
+      const char* f = cur.fptr((size_t)c);
+      const int64_t fl = cur.flen((size_t)c);
       double v;
       if (mode == 1 && fl == 2 && f[0] == 'N' && f[1] == 'A') {
         if (row < cap_rows) out[row * ncols + col] = __builtin_nan("");

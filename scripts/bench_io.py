@@ -44,7 +44,8 @@ with tempfile.TemporaryDirectory() as d:
     p.write_text(",".join(f"s{i}" for i in range(1024)) + "\n" +
                  "".join(",".join(repr(float(v)) for v in row) + "\n" for row in X.T))
     t0 = time.perf_counter(); P.load_csv(p); el_parse = time.perf_counter() - t0
-    t0 = time.perf_counter(); pio._load_csv_reference(p); el_parse_ref = time.perf_counter() - t0
+    # the reference algorithm, as restated in the oracle (csv module + float())
+    t0 = time.perf_counter(); O.load_csv_rows(p); el_parse_ref = time.perf_counter() - t0
     mb = p.stat().st_size / 1e6
 print(json.dumps({
     "write_skill_matrix": {"N": N, "cells_per_s": cells / el, "text_GB_per_s": nbytes / el / 1e9,
