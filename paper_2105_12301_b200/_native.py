@@ -139,3 +139,26 @@ def device_count() -> int:
     n = np.zeros(1, dtype=np.int32)
     check(load().cmb_device_count(ptr(n)))
     return int(n[0])
+
+
+_MADV_HUGEPAGE = 14
+_HUGE = 2 << 20
+
+
+def host_empty(shape, dtype) -> np.ndarray:
+    """np.empty for large result arrays, backed by transparent huge pages where the
+    kernel allows it (madvise mode): an N x N float32 cross map at N = 53,053 is
+    2.8 M 4 KB page faults on first touch, 5.5 k with 2 MB pages."""
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape)) * dtype.itemsize
+    if n < (64 << 20):
+        return np.empty(shape, dtype)
+    raw = np.empty(n + _HUGE, dtype=np.uint8)
+    off = (-raw.ctypes.data) % _HUGE
+    buf = raw[off:off + n]
+    try:
+        libc = C.CDLL(None, use_errno=True)
+        libc.madvise(C.c_void_p(buf.ctypes.data), C.c_size_t(n - n % _HUGE), _MADV_HUGEPAGE)
+    except (OSError, AttributeError):  # pragma: no cover - platform without madvise
+        pass
+    return buf.view(dtype).reshape(shape)

@@ -186,7 +186,7 @@ def xmap_multi(values: np.ndarray, estar, devices, tau: int = 1) -> np.ndarray:
     N, T = X.shape
     est = np.ascontiguousarray(estar, dtype=np.int32)
     devs = np.ascontiguousarray(devices, dtype=np.int32)
-    out = np.empty((N, N), dtype=np.float32)
+    out = nat.host_empty((N, N), np.float32)
     st = np.zeros(8)
     nat.call("cmb_xmap_multi", nat.ptr(devs), devs.size, nat.ptr(X), N, T, nat.ptr(est), tau, nat.ptr(out),
              nat.ptr(st))

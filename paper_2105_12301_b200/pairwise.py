@@ -126,7 +126,7 @@ def xmap(values, e_star, tau: int = 1, layout: int = LAYOUT_LIB_MAJOR, dtype=np.
     wide = (est > NATIVE_E_MAX) | ((T > NATIVE_T_MAX) & (est > 0))
     if wide.any():
         return _xmap_with_wide(np.ascontiguousarray(Xs, dtype=np.float32), est, wide, tau, layout, dtype, stats)
-    out = np.empty((N, N), dtype=np.float32)
+    out = nat.host_empty((N, N), np.float32)
     st = np.zeros(8)
     nat.call("cmb_xmap" if f32 else "cmb_xmap64", nat.device(), nat.ptr(Xs), N, T, nat.ptr(est), tau,
              nat.ptr(out), layout, nat.ptr(st))
@@ -156,8 +156,8 @@ def xmap_predictions(values, e_star, pairs, tau: int = 1) -> tuple[np.ndarray, n
     pl = np.ascontiguousarray([p[0] for p in pairs], dtype=np.int32)
     pt = np.ascontiguousarray([p[1] for p in pairs], dtype=np.int32)
     Xs = np.ascontiguousarray(X.T)
-    rho = np.empty((N, N), dtype=np.float32)
-    pred = np.empty((max(pl.size, 1), T), dtype=np.float32)
+    rho = nat.host_empty((N, N), np.float32)
+    pred = nat.host_empty((max(pl.size, 1), T), np.float32)
     nat.call("cmb_xmap_predict", nat.device(), nat.ptr(Xs), N, T, nat.ptr(est), tau, nat.ptr(pl), nat.ptr(pt),
              pl.size, nat.ptr(rho), LAYOUT_LIB_MAJOR, nat.ptr(pred), None)
     return rho, pred[: pl.size]
