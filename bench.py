@@ -368,10 +368,9 @@ def run_ours(args):
     os.environ["CMB_DEVICE"] = str(local)
     comm_info = None
     if world > 1 or native:
-        if native:
-            os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator lines (nranks) on stderr
-            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+        # the communicator's size is reported from ncclCommCount (`nccl` in the
+        # JSON line); NCCL_DEBUG is left to the caller so nothing but the JSON
+        # line reaches rank 0's stdout
         dist.init_process_group("gloo")
         if native:
             comm_info = init_native_comm(local)
