@@ -8,20 +8,28 @@
 // leaves the SM.
 //
 // B200 mapping.  A CTA keeps one block of 32 targets (all with the same E*)
-// resident in shared memory, time-major: tgt[t][lane] -- T = 1,450 samples x
-// 128 B = 185.6 KB of the 227 KB -- so every gathered row is one
-// conflict-free 128-byte shared-memory wavefront (lane = target).  Its 16
-// warps each stream their own libraries' neighbour tables (records of k
-// fp32 weights + k u16 rows) from L2/HBM into a 2-slot shared-memory ring
-// with cp.async.bulk (TMA bulk copies) completing on an mbarrier, so table
-// bytes are fetched once per (library, target block) and read back as
-// broadcast 16-byte shared loads.  Skill is accumulated per lane in fp32 over
-// a staging slot and folded into fp64; rho is evaluated in fp64 against the
-// precomputed observed-segment moments.
+// resident in shared memory, time-major: tgt[t][32] -- T = 1,450 samples x
+// 128 B = 185.6 KB of the 227 KB -- plus a zero row.  Its warps stream their
+// own libraries' neighbour tables (records of k fp32 weights + k u16 rows)
+// from L2/HBM into per-warp 2-slot shared-memory rings with cp.async.bulk
+// (TMA bulk copies) completing on mbarriers, so table bytes are fetched once
+// per (library, target block).  Work items are (E group, library sub-range,
+// target block), handed out by an atomic counter so concurrently running
+// CTAs share the same libraries' tables in L2.
 //
-// Work items are (E group, library sub-range, target block), handed out by
-// an atomic counter so concurrently running CTAs share the same libraries'
-// tables in L2.
+// The default (resident fp32) path is the rotated-lane layout
+// (rot_library_group / rot2_library_pairs below): a lane owns an embedded
+// point, loads its record once, and rotates over the block's target columns,
+// so every gather is one conflict-free wavefront and no record is broadcast;
+// the moments stay in registers for a whole library and are transposed once.
+// It runs as one launch per neighbour-count class (kernels.cuh
+// lookup_class_warps: 12 warps for k <= 16, 8 for 17..24, both on the
+// two-target path; 16 otherwise).  The lane = target layout with broadcast
+// records (warp_libraries / warp_library_group) remains for the non-resident
+// case (targets gathered from L2), the 16-bit target modes and fallbacks.
+// Skill is evaluated in fp64 against the precomputed observed-segment
+// moments; ill-conditioned pairs of the rotated path are finished in fp64 by
+// lookup_fixup_kernel.
 #pragma once
 
 #include "cmb_common.cuh"
