@@ -388,6 +388,7 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   CMB_CUDA(launch_build_targets(X, ld, ctx->buf[B_MEAN].as<double>(), ctx->buf[B_SLOT_TGT].as<int32_t>(),
                                 slots, (int)T, ctx->buf[B_Y].as<float>(), ldy, st));
   const bool h16 = want_h16 && stage != kNonResidentStage;
+  la.tmajor = !(getenv("CMB_LOOKUP_TMAJOR") && getenv("CMB_LOOKUP_TMAJOR")[0] == '0');
   if (h16) {
     for (int g = 0; g < la.ngroups; ++g) {  // blocks of 64 slots
       la.g_blk0[g] /= 2;
@@ -1433,6 +1434,7 @@ int cmb_ccm_convergence(int dev, const double* X, int64_t N, int64_t len, int E,
     la.rhoT = ctx->buf[B_RHOT].as<float>();
     la.ldr = ldr;
     la.stage_bytes = stage;
+    la.tmajor = 1;
     CMB_CUDA(cudaMemsetAsync(la.counter, 0, sizeof(int), st));
     CMB_CUDA(launch_lookup_xmap(la, (int)std::min<int64_t>(la.n_items, dev_sms), st));
     chunk_rho.resize((size_t)NT * ldr);

@@ -80,6 +80,7 @@ struct LookupArgs {
   // chunk, first slot of the block) and recomputed in fp64 by lookup_fixup_kernel
   int rot;
   int warps;                 // CTA warps of this launch (0 = kLookupWarps; 12 / 8: rot2 class kernels)
+  int tmajor;                // non-resident: work items target-block-major (CMB_LOOKUP_TMAJOR=0: library-major)
   double fix_ratio;          // queue when m2p <= fix_ratio * sum p^2
   int2* fix;
   int* fix_count;
@@ -87,6 +88,10 @@ struct LookupArgs {
 };
 
 constexpr int kLookupWarps = 16;
+// CTA warps of the non-resident (long-series) lookup: up to 255 registers per
+// thread (more gathers in flight per warp) and half the staging rings of 16
+// warps, so more of the SM's L1 caches target rows (K3-L2)
+constexpr int kNonResWarps = 8;
 // stage size that selects the non-resident (targets in L2) lookup variant
 constexpr int kNonResidentStage = 4096 + 16;
 int lookup_stage_bytes(int T, int max_rec_bytes, int warps = kLookupWarps);

@@ -47,7 +47,7 @@ cudaError_t launch_lookup_resident16(const LookupArgs& a, int grid, int smem, cu
 
 cudaError_t launch_lookup_xmap(const LookupArgs& a, int grid, cudaStream_t st) {
   const bool resident = a.stage_bytes != kNonResidentStage;
-  const int warps = (resident && !a.h16 && a.warps) ? a.warps : kLookupWarps;
+  const int warps = !resident ? kNonResWarps : ((!a.h16 && a.warps) ? a.warps : kLookupWarps);
   const int smem = (resident ? (a.T + 1) * 128 : 0) + warps * 2 * a.stage_bytes + warps * 2 * 8;
   count_launch();
   if (!resident) return launch_lookup_nonresident(a, grid, smem, st);

@@ -1205,8 +1205,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lookup_xmap_kernel(LookupArgs a
     while (g + 1 < a.ngroups && a.g_item0[g + 1] <= item) ++g;
     const int64_t rem = item - a.g_item0[g];
     const int nblk = a.g_nblk[g];
-    const int lsub = (int)(rem / nblk);
-    const int blk = a.g_blk0[g] + (int)(rem - (int64_t)lsub * nblk);
+    // resident: library-major items (concurrent CTAs share the libraries'
+    // tables in L2, each keeps its own target block in shared memory);
+    // non-resident: target-block-major (concurrent CTAs gather from the same
+    // target block in L2 and stream their own libraries' tables)
+    int lsub, blk;
+    if (RESIDENT || !a.tmajor) {
+      lsub = (int)(rem / nblk);
+      blk = a.g_blk0[g] + (int)(rem - (int64_t)lsub * nblk);
+    } else {
+      const int b = (int)(rem / a.n_lsub);
+      lsub = (int)(rem - (int64_t)b * a.n_lsub);
+      blk = a.g_blk0[g] + b;
+    }
     const int E = a.g_E[g];
 
     // stage the target block (32 fp32 or 64 fp16 targets: 128 bytes per row), time-major
@@ -1225,7 +1236,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lookup_xmap_kernel(LookupArgs a
     const int per_warp = a.LS / WARPS;
     const int lib0 = lsub * a.LS + w * per_warp;
     const int nl = max(0, min(per_warp, a.nlib - lib0));
-    if constexpr (WARPS != kLookupWarps) {
+    if constexpr (RESIDENT && WARPS != kLookupWarps) {
       // class kernels: the host only sends them k with a feasible two-target stage
       if (nl > 0) {
         switch (E + 1) {

@@ -4,10 +4,10 @@
 namespace cmb {
 
 cudaError_t launch_lookup_nonresident(const LookupArgs& a, int grid, int smem, cudaStream_t st) {
-  auto kern = lookup_xmap_kernel<false, 0>;
+  auto kern = lookup_xmap_kernel<false, 0, kNonResWarps>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  kern<<<grid, kLookupWarps * 32, smem, st>>>(a);
+  kern<<<grid, kNonResWarps * 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
