@@ -44,6 +44,20 @@ def test_xmap_long_series_non_resident_lookup():
     assert worst <= RHO_TOL, worst
 
 
+def test_non_resident_work_order_is_bitwise_neutral(monkeypatch):
+    """The long-series lookup hands out target-block-major work items
+    (LookupArgs::tmajor, DESIGN.md K3-L2); every (library, target) pair is still
+    computed by one warp in the same operation order, so rho equals the
+    library-major order bit for bit (T = 2,000: just past shared memory)."""
+    X = P.mixed_dataset(300, 2_000, seed=11, dtype=np.float32)
+    est = np.array([(1, 2, 4, 7, 12, 20)[i % 6] for i in range(300)], dtype=np.int32)
+    a = P.xmap(X.T, est, dtype=np.float32)
+    monkeypatch.setenv("CMB_LOOKUP_TMAJOR", "0")
+    b = P.xmap(X.T, est, dtype=np.float32)
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    assert np.array_equal(np.nan_to_num(a), np.nan_to_num(b))
+
+
 def test_edim_long_series_against_oracle():
     """Config 2's shape per series (T = 10,000, E = 1..20, Tp = 1): curves within
     1e-10 of the oracle's fp64 restatement and E* equal, on four series of
