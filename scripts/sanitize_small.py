@@ -19,7 +19,11 @@ os.environ["CMB_LOOKUP_FP16"] = "1"
 rho16 = P.xmap(X.T, e, dtype=np.float32)                  # fp16-target lookup
 os.environ.pop("CMB_LOOKUP_FP16")
 Xl = P.mixed_dataset(6, 7000, seed=6)                     # long series: non-resident lookup
-rl = P.xmap(Xl.T, [1, 2, 3, 2, 1, 4], dtype=np.float32)
+rl = P.xmap(Xl.T, [1, 2, 3, 2, 1, 4], dtype=np.float32)  # (target-block-major work items)
+os.environ["CMB_LOOKUP_TMAJOR"] = "0"                     # library-major order, same kernel
+rl0 = P.xmap(Xl.T, [1, 2, 3, 2, 1, 4], dtype=np.float32)
+os.environ.pop("CMB_LOOKUP_TMAJOR")
+assert np.array_equal(np.nan_to_num(rl), np.nan_to_num(rl0))
 t = P.build_knn_table(X[3], P.EmbeddingSpec(5, 1))        # RAW tile kernel
 t2 = P.build_knn_table(X[3], P.EmbeddingSpec(3, 2))       # RAW v4 (tau = 2)
 cv = P.ccm_sweep(X[:5].T, e[:5], [20, 80], samples=3)     # convergence tables + lookup
