@@ -7,6 +7,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <thread>
 #include <atomic>
 #include <cstdarg>
@@ -111,6 +112,10 @@ struct Ctx {
   HostBuf bounce[2];
   ncclComm_t comm = nullptr;  // cmb_nccl_init_rank / cmb_xmap_multi
   int nranks = 1, rank = 0;
+  // mapped page-locked word: per-chunk counters read back by a one-thread
+  // kernel, not a DMA copy, which would queue behind the chunk's rho D2H
+  int* cnt_host = nullptr;
+  int* cnt_dev = nullptr;
   bool ready = false;
 };
 
@@ -442,6 +447,10 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
   const char* fix_env = getenv("CMB_FIX_RATIO");
   const char* split_env = getenv("CMB_LOOKUP_SPLIT");  // 0: every k in one 16-warp launch
   CMB_CUDA(ctx->buf[B_FIX].ensure(16 + sizeof(int2) * (size_t)kFixCap));
+  if (!ctx->cnt_host) {
+    CMB_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->cnt_host), 64, cudaHostAllocMapped));
+    CMB_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->cnt_dev), ctx->cnt_host, 0));
+  }
   int64_t fixups = 0;
   EventSet evs;
   cudaEvent_t ev[3];
@@ -558,7 +567,10 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     };
     const bool split = !(split_env && split_env[0] == '0');
     CMB_TRY(launch_all(split));
-    if (la.rot) CMB_CUDA(launch_lookup_fixup(la, st));
+    if (la.rot) {
+      CMB_CUDA(launch_lookup_fixup(la, st));
+      CMB_CUDA(launch_copy_count(la.fix_count, ctx->cnt_dev, st));
+    }
     if (!pairs.empty()) {
       const auto lo_it = std::lower_bound(pairs.begin(), pairs.end(), (int)c0,
                                           [](const int4& a, int v) { return a.x < v; });
@@ -576,8 +588,10 @@ static int xmap_core(Ctx* ctx, cudaStream_t st, const float* X, int64_t N, int64
     CMB_CUDA(cudaEventRecord(ev[2], st));
     CMB_CUDA(cudaEventSynchronize(ev[2]));
     if (la.rot) {
-      int nfix = 0;
-      CMB_CUDA(cudaMemcpy(&nfix, la.fix_count, sizeof(int), cudaMemcpyDeviceToHost));
+      // written by launch_copy_count before ev[2]: no DMA copy, which would wait
+      // behind the previous chunks' rho copies on the D2H engine (host-buffer
+      // cross map) and leave the GPU idle until it returns
+      const int nfix = *reinterpret_cast<volatile int*>(ctx->cnt_host);
       fixups += nfix;
       if (nfix > kFixCap) {
         // more ill-conditioned pairs than the queue holds (a pathological chunk):
@@ -645,6 +659,8 @@ int cmb_shutdown(void) {
     cudaSetDevice(c->dev);
     for (auto& b : c->buf) b.release();
     for (auto& b : c->bounce) b.release();
+    if (c->cnt_host) cudaFreeHost(c->cnt_host);
+    c->cnt_host = c->cnt_dev = nullptr;
     if (c->comm) nccl_destroy(c->comm);
     c->comm = nullptr;
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -972,13 +988,21 @@ static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t
       slot ^= 1;
       return CMB_OK;
     };
+    const auto t_core0 = std::chrono::steady_clock::now();
     const int rc = xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
                              ctx->buf[B_RHOT].as<float>(), ldr, &s, on_chunk, x64, err, prp);
+    const auto t_core1 = std::chrono::steady_clock::now();
     cudaEvent_t copied;
     CMB_CUDA(evs.make(&copied, cudaEventDisableTiming));
     CMB_CUDA(cudaEventRecord(copied, ctx->copy_stream));
     CMB_CUDA(cudaStreamWaitEvent(st, copied, 0));
     CMB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+    if (getenv("CMB_TRACE")) {
+      const auto t_copy = std::chrono::steady_clock::now();
+      const auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      fprintf(stderr, "cmb_xmap trace: core %.1f ms (tables %.1f + lookup %.1f), copy tail %.1f ms\n",
+              ms(t_core0, t_core1), s.t_tables * 1e3, s.t_lookup * 1e3, ms(t_core1, t_copy));
+    }
     if (rc) return rc;
     CMB_TRY(drain());
   } else {

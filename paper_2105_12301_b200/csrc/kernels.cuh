@@ -147,6 +147,8 @@ cudaError_t launch_build_targets(const float* x32, int64_t ld, const double* mea
 cudaError_t launch_obs_moments(const float* Y, int64_t ldy, int T, int tau, const int32_t* slot_E,
                                int64_t slots, double* s, double* ss, uint8_t* cst, cudaStream_t st);
 cudaError_t launch_fill_nan(float* p, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st);
+// *dst = *src by one thread (dst: mapped page-locked host memory)
+cudaError_t launch_copy_count(const int* src, int* dst, cudaStream_t st);
 cudaError_t launch_targets_to_half(const float* Y, int64_t ldy, int T, int tau, const int32_t* slot_E,
                                    int64_t slots, void* Yh, double* s, double* ss, uint8_t* cst,
                                    int mode, cudaStream_t st);

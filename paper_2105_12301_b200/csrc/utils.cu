@@ -480,6 +480,14 @@ cudaError_t launch_targets_to_half(const float* Y, int64_t ldy, int T, int tau, 
   return cudaGetLastError();
 }
 
+__global__ void copy_count_kernel(const int* __restrict__ src, volatile int* dst) { *dst = *src; }
+
+cudaError_t launch_copy_count(const int* src, int* dst, cudaStream_t st) {
+  count_launch();
+  copy_count_kernel<<<1, 1, 0, st>>>(src, dst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill_nan(float* p, int64_t rows, int64_t cols, int64_t ld, cudaStream_t st) {
   if (rows * cols == 0) return cudaSuccess;
   count_launch();
