@@ -902,6 +902,8 @@ namespace cmb {
 // straight into rho_out when it is page-locked, else through two pinned
 // bounce slabs (a device-to-pageable copy would block the host and serialise
 // the chunks).
+constexpr int kDrainThreads = 8;  // host threads copying a bounce slab into pageable output
+
 static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t N, int64_t len,
                      const int32_t* estar, int tau, float* rho_out, int layout, double* stats_out,
                      const int32_t* pair_lib = nullptr, const int32_t* pair_tgt = nullptr, int64_t P = 0,
@@ -953,12 +955,47 @@ static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t
     struct Pending { int64_t lo = 0, hi = 0; float* slab = nullptr; cudaEvent_t ev = nullptr; };
     Pending pend;
     int slot = 0;
+    // pageable output: its pages are first touched (faulted and zeroed by the
+    // OS, ~1 s for the 11 GB of config 3) by host threads while the first chunk
+    // computes, not inside the drains; joined before the first drain writes
+    std::vector<std::thread> touch;
+    if (!pinned) {
+      const size_t bytes = sizeof(float) * (size_t)N * (size_t)N;
+      const size_t page = 4096;
+      for (int t = 0; t < kDrainThreads; ++t)
+        touch.emplace_back([=]() {
+          volatile char* b = reinterpret_cast<volatile char*>(rho_out);
+          for (size_t o = bytes * t / kDrainThreads / page * page; o < bytes * (t + 1) / kDrainThreads; o += page) b[o] = 0;
+        });
+    }
+    auto join_touch = [&]() {
+      for (auto& th : touch) th.join();
+      touch.clear();
+    };
     auto drain = [&]() -> int {
+      join_touch();
       if (!pend.slab) return CMB_OK;
+      const auto t0 = std::chrono::steady_clock::now();
       CMB_CUDA(cudaEventSynchronize(pend.ev));
+      const auto t1 = std::chrono::steady_clock::now();
       const int64_t w = pend.hi - pend.lo;
-      for (int64_t r = 0; r < N; ++r) memcpy(rho_out + r * N + pend.lo, pend.slab + r * w, sizeof(float) * w);
+      // row copies split over host threads (first touch of the caller's pages
+      // and the strided memcpy are both host-bound)
+      const float* slab = pend.slab;
+      const int64_t lo = pend.lo;
+      auto rows = [&](int64_t r0, int64_t r1) {
+        for (int64_t r = r0; r < r1; ++r) memcpy(rho_out + r * N + lo, slab + r * w, sizeof(float) * w);
+      };
+      const int nt = (int)std::min<int64_t>(kDrainThreads, std::max<int64_t>(1, N / 1024));
+      std::vector<std::thread> pool;
+      for (int t = 1; t < nt; ++t) pool.emplace_back(rows, N * t / nt, N * (t + 1) / nt);
+      rows(0, N / nt);
+      for (auto& th : pool) th.join();
       pend.slab = nullptr;
+      if (getenv("CMB_TRACE"))
+        fprintf(stderr, "cmb_xmap trace: drain cols %lld: wait %.1f ms, memcpy %.1f ms\n", (long long)w,
+                std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t1).count());
       return CMB_OK;
     };
     auto on_chunk = [&](int64_t lo, int64_t hi) -> int {
@@ -991,6 +1028,7 @@ static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t
     const auto t_core0 = std::chrono::steady_clock::now();
     const int rc = xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
                              ctx->buf[B_RHOT].as<float>(), ldr, &s, on_chunk, x64, err, prp);
+    join_touch();  // (an early error return from xmap_core skips the drains)
     const auto t_core1 = std::chrono::steady_clock::now();
     cudaEvent_t copied;
     CMB_CUDA(evs.make(&copied, cudaEventDisableTiming));
@@ -1004,7 +1042,11 @@ static int xmap_host(Ctx* ctx, cudaStream_t st, const void* X, bool f64, int64_t
               ms(t_core0, t_core1), s.t_tables * 1e3, s.t_lookup * 1e3, ms(t_core1, t_copy));
     }
     if (rc) return rc;
+    const auto t_drain0 = std::chrono::steady_clock::now();
     CMB_TRY(drain());
+    if (getenv("CMB_TRACE"))
+      fprintf(stderr, "cmb_xmap trace: pageable=%d last drain %.1f ms\n", (int)!pinned,
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_drain0).count());
   } else {
     CMB_TRY(xmap_core(ctx, st, ctx->buf[B_X32].as<float>(), N, len, len, estar, tau, 0, N,
                       ctx->buf[B_RHOT].as<float>(), ldr, &s, nullptr, x64, err, prp));
