@@ -130,9 +130,16 @@ static __device__ __noinline__ void lane_min_thresholds(const float* mins, float
       }
     }
     const int kp = kp_of(mode, k_raw, L, 1, e);
-    float t = v[0];
+    // t = v[kp - 1] by a select tree over the bits of kp - 1 (five dependent
+    // levels instead of a 31-step chain; ncu: the chain was 2.6% of the stalls)
+    const int q1 = kp - 1;
 #pragma unroll
-    for (int q = 1; q < 32; ++q) t = (q == kp - 1) ? v[q] : t;
+    for (int lv = 0; lv < 5; ++lv) {
+      const bool hi = (q1 >> lv) & 1;
+#pragma unroll
+      for (int q = 0; q < (32 >> (lv + 1)); ++q) v[q] = hi ? v[2 * q + 1] : v[2 * q];
+    }
+    const float t = v[0];
     const float tn = (t < kInfF) ? -__int_as_float(__float_as_int(t) + 1) : -kInfF;
     thr[e] = t;
     ntp[e] = make_float2(tn, tn);
