@@ -27,6 +27,8 @@ SOURCES = ["knn_sweep.cu", "knn_w_a.cu", "knn_w_b.cu", "knn_w_c.cu", "knn_w_d.cu
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", f"-I{CSRC}"]
+if os.environ.get("CMB_NR_WARPS"):  # A/B builds: CTA warps of the non-resident lookup
+    FLAGS.append("-DCMB_NR_WARPS=" + os.environ["CMB_NR_WARPS"])
 if os.environ.get("CMB_STATS") == "1":  # selection counters in diagnostics[3..5] (profiling builds only)
     FLAGS.append("-DCMB_KNN_STATS")
 

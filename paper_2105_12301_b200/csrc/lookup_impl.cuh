@@ -1233,9 +1233,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lookup_xmap_kernel(LookupArgs a
     }
     __syncthreads();
 
-    const int per_warp = a.LS / WARPS;
+    // the item's libraries [lsub LS, (lsub + 1) LS) split over the warps (LS need
+    // not be a multiple of WARPS)
+    const int per_warp = (a.LS + WARPS - 1) / WARPS;
     const int lib0 = lsub * a.LS + w * per_warp;
-    const int nl = max(0, min(per_warp, a.nlib - lib0));
+    const int nl = max(0, min(per_warp, min(a.nlib, (lsub + 1) * a.LS) - lib0));
     if constexpr (RESIDENT && WARPS != kLookupWarps) {
       // class kernels: the host only sends them k with a feasible two-target stage
       if (nl > 0) {
