@@ -1233,11 +1233,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1) lookup_xmap_kernel(LookupArgs a
     }
     __syncthreads();
 
-    // the item's libraries [lsub LS, (lsub + 1) LS) split over the warps (LS need
-    // not be a multiple of WARPS)
-    const int per_warp = (a.LS + WARPS - 1) / WARPS;
-    const int lib0 = lsub * a.LS + w * per_warp;
-    const int nl = max(0, min(per_warp, min(a.nlib, (lsub + 1) * a.LS) - lib0));
+    // the item's libraries [lsub LS, (lsub + 1) LS) split over the warps (the
+    // non-resident kernel's warp count need not divide LS)
+    int per_warp, nl, lib0;
+    if constexpr (RESIDENT) {
+      per_warp = a.LS / WARPS;
+      lib0 = lsub * a.LS + w * per_warp;
+      nl = max(0, min(per_warp, a.nlib - lib0));
+    } else {
+      per_warp = (a.LS + WARPS - 1) / WARPS;
+      lib0 = lsub * a.LS + w * per_warp;
+      nl = max(0, min(per_warp, min(a.nlib, (lsub + 1) * a.LS) - lib0));
+    }
     if constexpr (RESIDENT && WARPS != kLookupWarps) {
       // class kernels: the host only sends them k with a feasible two-target stage
       if (nl > 0) {
